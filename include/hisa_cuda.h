@@ -1,0 +1,197 @@
+/* hisa_cuda.h — C ABI of the B200 (sm_100a) hierarchical-indexer library.
+ *
+ * This is the drop-in boundary for the reference's indexer hot path (reference tree: proj/core, headers
+ * only).  The reference has no FFI of its own; each entry point below names the reference C++ interface
+ * it replaces, batched over all query rows because a per-row device call is meaningless:
+ *
+ *   hisa_cuda_upload_keys / _pool_build / _pool_append / _pool_read
+ *        <- hisa::build_block_summaries, BlockSummaryCache::append / pooled / count
+ *           (proj/core/include/hisa/block_summary.hpp:23-59)
+ *   hisa_cuda_score_blocks       <- hisa::score_blocks      (hisa/hisa.hpp:16-21)
+ *   hisa_cuda_select_blocks      <- hisa::select_blocks     (hisa/hisa.hpp:23-28)
+ *   hisa_cuda_score_tokens       <- hisa::score_tokens      (hisa/dsa.hpp:13-20)
+ *   hisa_cuda_top_k              <- hisa::top_k_tokens      (hisa/dsa.hpp:22-27)
+ *   hisa_cuda_hisa_select        <- hisa::hisa_select       (hisa/hisa.hpp:35-45) incl. candidate_union (:30-33)
+ *   hisa_cuda_dsa_select         <- hisa::dsa_select        (hisa/dsa.hpp:29-32)
+ *   hisa_cuda_block_sparse_select<- hisa::block_sparse_select (hisa/block_sparse.hpp:12-19)
+ *   hisa_cuda_config             <- hisa::HisaConfig        (hisa/config.hpp:26-67), POD mirror
+ *   status codes                 <- the exception leaves of hisa/errors.hpp:10-28
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no C++ or torch types cross this boundary.
+ *   - data pointers may be HOST or DEVICE memory (detected with cudaPointerGetAttributes); host buffers
+ *     are copied inside the call (pinned memory from hisa_cuda_host_alloc makes those copies asynchronous).
+ *   - nothing throws: every function returns a hisa_status; hisa_cuda_last_error gives the message.
+ *   - there is NO CPU fallback: without a usable sm_100 device hisa_cuda_create fails with
+ *     HISA_ERR_NO_DEVICE and nothing else can be called.
+ *   - a context is bound to one device and one stream and is not thread-safe; use one per GPU.
+ *   - selection output is a fixed int32 [Q, token_budget] matrix: the first out_count[row] entries of a
+ *     row are the selected token positions in ascending order, the rest is padded with -1.
+ */
+#ifndef HISA_CUDA_H_
+#define HISA_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HISA_CUDA_ABI_VERSION 1
+
+typedef struct hisa_cuda_ctx hisa_cuda_ctx;
+
+typedef enum hisa_status {
+  HISA_OK = 0,
+  HISA_ERR_INFEASIBLE_CONFIG = 1,  /* hisa::InfeasibleConfig */
+  HISA_ERR_CAUSAL_VIOLATION = 2,   /* hisa::CausalViolation */
+  HISA_ERR_EMPTY_SEQUENCE = 3,     /* hisa::EmptySequence */
+  HISA_ERR_DIMENSION_MISMATCH = 4, /* hisa::DimensionMismatch */
+  HISA_ERR_NON_FINITE = 5,         /* hisa::NonFiniteValue */
+  HISA_ERR_SHAPE_MISMATCH = 6,     /* hisa::ShapeMismatch */
+  HISA_ERR_EMPTY_SELECTION = 7,    /* hisa::EmptySelection */
+  HISA_ERR_INVALID_ARGUMENT = 8,
+  HISA_ERR_UNSUPPORTED = 9,        /* shape outside what the sm_100a kernels cover (H > 64, d > 128, ...) */
+  HISA_ERR_NO_DEVICE = 10,         /* no CUDA device / not sm_100: there is no CPU fallback */
+  HISA_ERR_CUDA = 11,              /* a CUDA runtime/driver call failed; message has the detail */
+  HISA_ERR_OUT_OF_MEMORY = 12
+} hisa_status;
+
+typedef enum hisa_dtype {
+  HISA_DTYPE_F32 = 0,  /* float32 storage; scored with exact 3-way bf16 splits (fp32-grade products) */
+  HISA_DTYPE_BF16 = 1  /* bfloat16 storage, the production format */
+} hisa_dtype;
+
+typedef enum hisa_tie_break { HISA_TIE_SMALLEST_INDEX = 0, HISA_TIE_LARGEST_INDEX = 1 } hisa_tie_break;
+typedef enum hisa_pool_mode { HISA_POOL_MEAN = 0, HISA_POOL_MAX = 1 } hisa_pool_mode;
+
+/* scorer implementation: the tcgen05/TMA kernel is the product path; the SIMT kernel is a slow
+ * device-side cross-check used by the tests (still CUDA, never the CPU). */
+typedef enum hisa_scorer { HISA_SCORER_TENSOR = 0, HISA_SCORER_SIMT = 1 } hisa_scorer;
+
+/* POD mirror of hisa::HisaConfig (hisa/config.hpp:47-66) plus the storage dtype of q and k. */
+typedef struct hisa_cuda_config {
+  uint32_t block_size;    /* B */
+  uint32_t block_budget;  /* m */
+  uint32_t token_budget;  /* k */
+  uint32_t num_heads;     /* H_I  (<= 64) */
+  uint32_t dim;           /* d    (<= 128) */
+  uint8_t force_first_last; /* default 1 */
+  uint8_t forced_in_budget; /* default 0 */
+  uint8_t tie_break;        /* hisa_tie_break */
+  uint8_t pool_mode;        /* hisa_pool_mode */
+  uint32_t dtype;           /* hisa_dtype of queries and keys */
+  uint32_t scorer;          /* hisa_scorer */
+  uint32_t reserved[4];     /* must be zero */
+} hisa_cuda_config;
+
+/* fills the defaults of hisa::HisaConfig for the given sizes */
+void hisa_cuda_config_init(hisa_cuda_config* cfg, uint32_t block_size, uint32_t block_budget,
+                           uint32_t token_budget, uint32_t num_heads, uint32_t dim, uint32_t dtype);
+
+/* same rule as the HisaConfig constructor (config.hpp:34-44): all fields > 0 and m*B >= k */
+int hisa_cuda_config_validate(const hisa_cuda_config* cfg);
+
+int hisa_cuda_abi_version(void);
+const char* hisa_cuda_status_name(int status);
+/* message of the last failure on this context; ctx == NULL reads the calling thread's global slot
+ * (used by hisa_cuda_create failures). The pointer stays valid until the next call on that ctx/thread. */
+const char* hisa_cuda_last_error(const hisa_cuda_ctx* ctx);
+
+int hisa_cuda_device_count(int* count);
+int hisa_cuda_create(int device, const hisa_cuda_config* cfg, hisa_cuda_ctx** out);
+int hisa_cuda_destroy(hisa_cuda_ctx* ctx);
+int hisa_cuda_synchronize(hisa_cuda_ctx* ctx);
+/* the CUDA stream (cudaStream_t) all work of this context is enqueued on */
+void* hisa_cuda_stream(hisa_cuda_ctx* ctx);
+
+/* pinned host memory for asynchronous host<->device copies */
+int hisa_cuda_host_alloc(void** ptr, size_t bytes);
+int hisa_cuda_host_free(void* ptr);
+/* plain device memory helpers so non-CUDA hosts (ctypes, cgo, JNI) can stage data themselves */
+int hisa_cuda_device_alloc(hisa_cuda_ctx* ctx, void** ptr, size_t bytes);
+int hisa_cuda_device_free(hisa_cuda_ctx* ctx, void* ptr);
+int hisa_cuda_memcpy(hisa_cuda_ctx* ctx, void* dst, const void* src, size_t bytes);
+
+/* ---- keys and block summaries ------------------------------------------------------------------ */
+/* Replaces the sequence with `seq_len` keys [seq_len, dim] of the context dtype. EmptySequence if 0.
+ * check_finite != 0 additionally scans for NaN/Inf (IndexerInputs ingestion rule, inputs.hpp:15-16). */
+int hisa_cuda_upload_keys(hisa_cuda_ctx* ctx, const void* keys, uint64_t seq_len, int check_finite);
+/* (Re)builds all block summaries of the current sequence: build_block_summaries. */
+int hisa_cuda_pool_build(hisa_cuda_ctx* ctx);
+/* Appends n keys [n, key_dim] at positions seq_len.. and updates only the touched tail blocks
+ * (BlockSummaryCache::append, n times, in position order). DimensionMismatch if key_dim != dim. */
+int hisa_cuda_pool_append(hisa_cuda_ctx* ctx, const void* keys, uint64_t n, uint32_t key_dim);
+/* Reads summaries back: sums [num_blocks, dim] (double), counts [num_blocks], pooled [num_blocks, dim]
+ * (double, = sum/count for Mean). Any output may be NULL. */
+int hisa_cuda_pool_read(hisa_cuda_ctx* ctx, double* sums, uint32_t* counts, double* pooled);
+int hisa_cuda_seq_len(const hisa_cuda_ctx* ctx, uint64_t* seq_len, uint64_t* num_blocks);
+
+/* ---- batched selection ------------------------------------------------------------------------- */
+/* queries [Q, H, d] (ctx dtype), gates [Q, H] float32, positions [Q] uint32 (each <= seq_len).
+ * out_idx     int32  [Q, token_budget]      ascending, -1 padded            (required)
+ * out_count   uint32 [Q]                    = min(k, candidate_size)        (optional)
+ * out_blocks  int32  [Q, block_budget + 2]  selected blocks ascending, -1 padded (optional; hisa only)
+ * out_nblocks uint32 [Q]                                                     (optional)
+ * out_cand    uint32 [Q]                    candidate_size = |Omega_t| (hisa) or t+1 (dsa) (optional)
+ * check_finite != 0 scans queries/gates for NaN/Inf first (costs one extra pass). */
+int hisa_cuda_hisa_select(hisa_cuda_ctx* ctx, const void* queries, const float* gates,
+                          const uint32_t* positions, uint64_t num_queries, int check_finite,
+                          int32_t* out_idx, uint32_t* out_count, int32_t* out_blocks,
+                          uint32_t* out_nblocks, uint32_t* out_cand);
+int hisa_cuda_dsa_select(hisa_cuda_ctx* ctx, const void* queries, const float* gates,
+                         const uint32_t* positions, uint64_t num_queries, int check_finite,
+                         int32_t* out_idx, uint32_t* out_count, uint32_t* out_cand);
+/* Stage 1 only: out_idx is int32 [Q, (block_budget+2)*block_size], all causally valid tokens of the
+ * selected blocks, ascending, -1 padded. */
+int hisa_cuda_block_sparse_select(hisa_cuda_ctx* ctx, const void* queries, const float* gates,
+                                  const uint32_t* positions, uint64_t num_queries, int check_finite,
+                                  int32_t* out_idx, uint32_t* out_count, int32_t* out_blocks,
+                                  uint32_t* out_nblocks);
+
+/* ---- single stages (for per-operation parity tests and callers that compose stages) ------------- */
+/* J[row, b] for b in [0, floor(t/B)] (eligible blocks); out_scores float32 [Q, num_blocks], entries of
+ * non-eligible blocks are unspecified; out_neligible uint32 [Q]. */
+int hisa_cuda_score_blocks(hisa_cuda_ctx* ctx, const void* queries, const float* gates,
+                           const uint32_t* positions, uint64_t num_queries, float* out_scores,
+                           uint32_t* out_neligible);
+/* select_blocks on caller-provided block scores: scores float32 [Q, score_stride], the first
+ * neligible[row] entries of a row are the eligible blocks 0..E-1. out_blocks int32 [Q, m+2]. */
+int hisa_cuda_select_blocks(hisa_cuda_ctx* ctx, const float* scores, uint64_t score_stride,
+                            const uint32_t* neligible, uint64_t num_queries, int32_t* out_blocks,
+                            uint32_t* out_nblocks);
+/* score_tokens for the whole causal prefix of each row: out_scores float32 [Q, out_stride] with
+ * out_stride >= round_up(seq_len, 128); entries beyond t are unspecified. CausalViolation cannot
+ * occur by construction (the prefix is generated, not passed in). */
+int hisa_cuda_score_tokens(hisa_cuda_ctx* ctx, const void* queries, const float* gates,
+                           const uint32_t* positions, uint64_t num_queries, float* out_scores,
+                           uint64_t out_stride);
+/* top_k_tokens on caller-provided scores: row r holds n[r] candidates at positions 0..n[r]-1.
+ * out_idx int32 [Q, k]. */
+int hisa_cuda_top_k(hisa_cuda_ctx* ctx, const float* scores, uint64_t score_stride, const uint32_t* n,
+                    uint64_t num_rows, uint32_t k, int32_t* out_idx, uint32_t* out_count);
+
+/* ---- instrumentation --------------------------------------------------------------------------- */
+typedef struct hisa_cuda_stage_times {
+  float prepare_ms;      /* dtype conversion / padding of q and w */
+  float score_blocks_ms; /* stage 1 scorer (tcgen05)  */
+  float select_blocks_ms;/* top-m + forced blocks     */
+  float invert_ms;       /* per-block query lists     */
+  float score_tokens_ms; /* stage 2 / flat scorer (tcgen05) */
+  float top_k_ms;        /* final top-k               */
+  float total_ms;        /* first kernel to last kernel of the call */
+  uint64_t launches;     /* kernels launched by the call */
+  uint64_t work_items_stage1, work_items_stage2; /* scorer work items (tile x query-list units) */
+} hisa_cuda_stage_times;
+/* enable != 0: record CUDA events around every stage of subsequent calls (adds a few us). */
+int hisa_cuda_set_profiling(hisa_cuda_ctx* ctx, int enable);
+/* times of the last select call; synchronizes the context's stream. */
+int hisa_cuda_last_stage_times(hisa_cuda_ctx* ctx, hisa_cuda_stage_times* out);
+/* total kernels launched on this context since creation */
+int hisa_cuda_launch_count(const hisa_cuda_ctx* ctx, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HISA_CUDA_H_ */

@@ -1,0 +1,1127 @@
+// Context + C ABI implementation (include/hisa_cuda.h). Host-side orchestration only: every arithmetic
+// step of the indexer runs in the CUDA kernels of pool.cu / score_tc.cu / select.cu. There is no CPU
+// fallback anywhere in this file: a missing device or a failed launch is an error.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hisa_cuda.h"
+#include "kernels.cuh"
+
+using namespace hisa_dev;
+
+namespace {
+
+thread_local std::string g_global_error;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+enum Stage { kStPrepare = 0, kStScoreBlocks, kStSelectBlocks, kStInvert, kStScoreTokens, kStTopK, kNumStages };
+
+struct StageSpan {
+  int stage;
+  cudaEvent_t beg, end;
+};
+
+}  // namespace
+
+struct hisa_cuda_ctx {
+  hisa_cuda_config cfg{};
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  // operand geometry
+  uint32_t nseg_k = 1, nseg_q = 1, nseg_p = 2;
+  uint32_t terms_tok[kMaxSeg] = {1, 0, 0};
+  uint32_t terms_blk[kMaxSeg] = {3, 0, 0};
+  bool q_zero_copy = false;  // caller's q already is the operand (bf16, H=64, d=128)
+
+  // sequence state
+  uint64_t seq_len = 0, key_cap = 0;
+  uint64_t pooled_tokens = 0;  // tokens folded into the summaries so far
+  DevBuf key_op, key_raw, sums, counts, pooled_op;
+
+  // per-call workspace
+  DevBuf q_raw, q_op, gates_raw, gates_pad, pos, J, sel, nsel, work, pairs, scalars, cand, flat, out_idx, out_count,
+      out_cand, generic_scores, generic_n, export_a, export_b, flag;
+
+  // tuning
+  uint32_t chunk_dense = 256, chunk_list = 512;
+  uint64_t workspace_bytes = 4ull << 30;
+
+  // instrumentation
+  bool profiling = false;
+  std::vector<StageSpan> spans;
+  std::vector<cudaEvent_t> event_pool;
+  size_t events_used = 0;
+  uint64_t launches = 0, call_launches = 0;
+  uint64_t items1 = 0, items2 = 0;
+  cudaEvent_t call_beg = nullptr, call_end = nullptr;
+
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+};
+
+namespace {
+
+int fail(hisa_cuda_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  else g_global_error = buf;
+  return code;
+}
+
+#define CU_TRY(ctx, expr)                                                                                   \
+  do {                                                                                                      \
+    cudaError_t e__ = (expr);                                                                               \
+    if (e__ != cudaSuccess)                                                                                 \
+      return fail(ctx, e__ == cudaErrorMemoryAllocation ? HISA_ERR_OUT_OF_MEMORY : HISA_ERR_CUDA,           \
+                  "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e__), __FILE__, __LINE__);             \
+  } while (0)
+
+#define HISA_TRY(expr)            \
+  do {                            \
+    int rc__ = (expr);            \
+    if (rc__ != HISA_OK) return rc__; \
+  } while (0)
+
+int ensure(hisa_cuda_ctx* ctx, DevBuf& b, size_t bytes) {
+  if (bytes <= b.cap) return HISA_OK;
+  if (b.p) {
+    CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    CU_TRY(ctx, cudaFree(b.p));
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  const size_t want = (bytes + 255) & ~size_t(255);
+  CU_TRY(ctx, cudaMalloc(&b.p, want));
+  b.cap = want;
+  return HISA_OK;
+}
+
+void release(DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+uint32_t elem_bytes(const hisa_cuda_ctx* ctx) { return ctx->cfg.dtype == HISA_DTYPE_BF16 ? 2u : 4u; }
+uint32_t round_up(uint32_t v, uint32_t m) { return (v + m - 1) / m * m; }
+uint64_t round_up64(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
+
+cudaEvent_t next_event(hisa_cuda_ctx* ctx) {
+  if (ctx->events_used == ctx->event_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->event_pool.push_back(e);
+  }
+  return ctx->event_pool[ctx->events_used++];
+}
+
+struct StageTimer {
+  hisa_cuda_ctx* ctx;
+  StageSpan span{};
+  bool on;
+  StageTimer(hisa_cuda_ctx* c, int stage) : ctx(c), on(c->profiling) {
+    if (on) {
+      span.stage = stage;
+      span.beg = next_event(ctx);
+      span.end = next_event(ctx);
+      cudaEventRecord(span.beg, ctx->stream);
+    }
+  }
+  ~StageTimer() {
+    if (on) {
+      cudaEventRecord(span.end, ctx->stream);
+      ctx->spans.push_back(span);
+    }
+  }
+};
+
+void count_launches(hisa_cuda_ctx* ctx, int n) {
+  ctx->launches += uint64_t(n);
+  ctx->call_launches += uint64_t(n);
+}
+
+int check_launch(hisa_cuda_ctx* ctx, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, HISA_ERR_CUDA, "launch of %s failed: %s", what, cudaGetErrorString(e));
+  return HISA_OK;
+}
+
+int make_map(hisa_cuda_ctx* ctx, CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  cuuint64_t gdim[2] = {cols, rows ? rows : 1};
+  cuuint64_t gstride[1] = {cols * sizeof(__nv_bfloat16)};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box,
+                           estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(ctx, HISA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu base=%p", int(r),
+                (unsigned long long)rows, (unsigned long long)cols, base);
+  return HISA_OK;
+}
+
+uint64_t num_blocks_of(const hisa_cuda_ctx* ctx) {
+  return (ctx->seq_len + ctx->cfg.block_size - 1) / ctx->cfg.block_size;
+}
+
+// ------------------------------------------------------------------------------------------------
+// prepared per-call inputs (device pointers valid until the next call on the context)
+// ------------------------------------------------------------------------------------------------
+struct Prepared {
+  const __nv_bfloat16* q_op = nullptr;  // [Q*64, nseg_q*128]
+  const float* gates = nullptr;         // [Q, 64]
+  const uint32_t* pos = nullptr;        // [Q]
+  uint64_t Q = 0;
+};
+
+int copy_in(hisa_cuda_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return HISA_OK;
+  CU_TRY(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+  return HISA_OK;
+}
+
+int read_flag(hisa_cuda_ctx* ctx, uint32_t* value) {
+  CU_TRY(ctx, cudaMemcpyAsync(value, ctx->flag.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return HISA_OK;
+}
+
+int prepare_inputs(hisa_cuda_ctx* ctx, const void* queries, const float* gates, const uint32_t* positions,
+                   uint64_t Q, int check_finite, Prepared* out) {
+  if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "selection over an empty key sequence");
+  if (Q == 0) {
+    out->Q = 0;
+    return HISA_OK;
+  }
+  if (!queries || !gates || !positions)
+    return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "queries, gates and positions must be non-null");
+  if (Q > 0x7FFFFFFFull / kHeads) return fail(ctx, HISA_ERR_UNSUPPORTED, "too many query rows in one call");
+  StageTimer timer(ctx, kStPrepare);
+  const uint32_t H = ctx->cfg.num_heads, d = ctx->cfg.dim, eb = elem_bytes(ctx);
+  const bool bf16 = ctx->cfg.dtype == HISA_DTYPE_BF16;
+
+  // positions
+  const uint32_t* pos_dev = positions;
+  if (!is_device_ptr(positions)) {
+    HISA_TRY(ensure(ctx, ctx->pos, Q * sizeof(uint32_t)));
+    HISA_TRY(copy_in(ctx, ctx->pos.p, positions, Q * sizeof(uint32_t)));
+    pos_dev = ctx->pos.as<uint32_t>();
+  }
+  // queries
+  const size_t q_elems = size_t(Q) * H * d;
+  const void* q_dev = queries;
+  if (!is_device_ptr(queries)) {
+    DevBuf& dst = ctx->q_zero_copy ? ctx->q_op : ctx->q_raw;
+    HISA_TRY(ensure(ctx, dst, q_elems * eb));
+    HISA_TRY(copy_in(ctx, dst.p, queries, q_elems * eb));
+    q_dev = dst.p;
+  }
+  // gates
+  const float* g_dev = gates;
+  if (!is_device_ptr(gates)) {
+    DevBuf& dst = (H == kHeads) ? ctx->gates_pad : ctx->gates_raw;
+    HISA_TRY(ensure(ctx, dst, size_t(Q) * H * sizeof(float)));
+    HISA_TRY(copy_in(ctx, dst.p, gates, size_t(Q) * H * sizeof(float)));
+    g_dev = dst.as<float>();
+  }
+  if (check_finite) {
+    HISA_TRY(ensure(ctx, ctx->flag, 16));
+    CU_TRY(ctx, cudaMemsetAsync(ctx->flag.p, 0, 16, ctx->stream));
+    uint32_t* f = ctx->flag.as<uint32_t>();
+    count_launches(ctx, launch_check_finite(q_dev, bf16, q_elems, f, ctx->stream));
+    count_launches(ctx, launch_check_finite(g_dev, 0, size_t(Q) * H, f + 1, ctx->stream));
+    count_launches(ctx, launch_check_positions(pos_dev, Q, uint32_t(ctx->seq_len), f + 2, ctx->stream));
+    uint32_t flags[3];
+    CU_TRY(ctx, cudaMemcpyAsync(flags, f, sizeof flags, cudaMemcpyDeviceToHost, ctx->stream));
+    CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (flags[0]) return fail(ctx, HISA_ERR_NON_FINITE, "inputs: non-finite value in queries");
+    if (flags[1]) return fail(ctx, HISA_ERR_NON_FINITE, "inputs: non-finite value in gates");
+    if (flags[2]) return fail(ctx, HISA_ERR_SHAPE_MISMATCH, "inputs: a query position exceeds the sequence length %llu",
+                              (unsigned long long)ctx->seq_len);
+  }
+  // operands
+  if (ctx->q_zero_copy) {
+    out->q_op = static_cast<const __nv_bfloat16*>(q_dev);
+  } else {
+    HISA_TRY(ensure(ctx, ctx->q_op, size_t(Q) * kHeads * ctx->nseg_q * kDim * sizeof(__nv_bfloat16)));
+    count_launches(ctx, launch_convert_rows(q_dev, bf16, Q, H, d, ctx->nseg_q, ctx->q_op.as<__nv_bfloat16>(), kHeads,
+                                            ctx->stream));
+    out->q_op = ctx->q_op.as<__nv_bfloat16>();
+  }
+  if (H == kHeads) {
+    out->gates = g_dev;
+  } else {
+    HISA_TRY(ensure(ctx, ctx->gates_pad, size_t(Q) * kHeads * sizeof(float)));
+    count_launches(ctx, launch_pad_gates(g_dev, Q, H, ctx->gates_pad.as<float>(), ctx->stream));
+    out->gates = ctx->gates_pad.as<float>();
+  }
+  out->pos = pos_dev;
+  out->Q = Q;
+  return check_launch(ctx, "input preparation");
+}
+
+// ------------------------------------------------------------------------------------------------
+// scorer dispatch
+// ------------------------------------------------------------------------------------------------
+struct ScoreJob {
+  const __nv_bfloat16* a_op;
+  uint64_t a_rows;
+  uint32_t nseg_a;
+  const uint32_t* terms;
+  const __nv_bfloat16* q_op;  // rows [0, nq*64)
+  uint64_t nq;
+  const float* gates;
+  float* out;
+  uint64_t out_stride;
+  bool list_mode;
+  const uint2* pairs;
+  uint32_t max_items;
+};
+
+int run_scorer(hisa_cuda_ctx* ctx, const ScoreJob& j) {
+  ScoreArgs a{};
+  uint32_t* sc = ctx->scalars.as<uint32_t>();
+  a.work = ctx->work.as<WorkItem>();
+  a.work_count = sc;
+  a.work_cursor = sc + 1;
+  a.pairs = j.pairs;
+  a.gates = j.gates;
+  a.out = j.out;
+  a.out_stride = j.out_stride;
+  a.list_mode = j.list_mode ? 1u : 0u;
+  const uint32_t B = ctx->cfg.block_size;
+  a.segs_per_block = j.list_mode ? (B + kTileRows - 1) / kTileRows : 1u;
+  a.block_rows = j.list_mode ? B : uint32_t(kTileRows);
+  a.nseg_a = j.nseg_a;
+  a.nseg_b = ctx->nseg_q;
+  for (int i = 0; i < kMaxSeg; ++i) a.terms[i] = j.terms[i];
+  a.a_rows = uint32_t(j.a_rows);
+  if (ctx->cfg.scorer == HISA_SCORER_SIMT) {
+    count_launches(ctx, launch_score_simt(a, j.a_op, j.q_op, j.max_items, ctx->stream));
+  } else {
+    CUtensorMap map_a, map_b;
+    HISA_TRY(make_map(ctx, &map_a, j.a_op, j.a_rows, uint64_t(j.nseg_a) * kDim, kTileRows));
+    HISA_TRY(make_map(ctx, &map_b, j.q_op, j.nq * kHeads, uint64_t(ctx->nseg_q) * kDim, kHeads));
+    count_launches(ctx, launch_score_tc(a, map_a, map_b, ctx->num_sms, ctx->stream));
+  }
+  return check_launch(ctx, "scorer");
+}
+
+int ensure_pool(hisa_cuda_ctx* ctx) {
+  if (ctx->pooled_tokens == ctx->seq_len) return HISA_OK;
+  return hisa_cuda_pool_build(ctx);
+}
+
+// stage 1: J[q, b] for rows [0, nq) -> ctx->J with stride Mpad
+int run_score_blocks(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, uint64_t nq, uint32_t Mpad) {
+  const uint32_t M = uint32_t(num_blocks_of(ctx));
+  const uint32_t ntiles = Mpad / kTileRows;
+  const uint32_t nchunks = uint32_t((nq + ctx->chunk_dense - 1) / ctx->chunk_dense);
+  HISA_TRY(ensure(ctx, ctx->work, size_t(nchunks) * ntiles * sizeof(WorkItem)));
+  HISA_TRY(ensure(ctx, ctx->J, size_t(nq) * Mpad * sizeof(float)));
+  uint32_t* sc = ctx->scalars.as<uint32_t>();
+  StageTimer timer(ctx, kStScoreBlocks);
+  count_launches(ctx, launch_build_dense_work(p.pos + q0, uint32_t(nq), ctx->chunk_dense, uint32_t(ctx->seq_len),
+                                              ctx->cfg.block_size, ntiles, ctx->work.as<WorkItem>(), sc, sc + 1,
+                                              ctx->stream));
+  ScoreJob j{};
+  j.a_op = ctx->pooled_op.as<__nv_bfloat16>();
+  j.a_rows = M;
+  j.nseg_a = ctx->nseg_p;
+  j.terms = ctx->terms_blk;
+  j.q_op = p.q_op + q0 * kHeads * ctx->nseg_q * kDim;
+  j.nq = nq;
+  j.gates = p.gates + q0 * kHeads;
+  j.out = ctx->J.as<float>();
+  j.out_stride = Mpad;
+  j.list_mode = false;
+  j.max_items = nchunks * ntiles;
+  ctx->items1 += j.max_items;
+  return run_scorer(ctx, j);
+}
+
+int run_select_blocks(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, uint64_t nq, uint32_t Mpad, int32_t* sel,
+                      uint32_t* nsel) {
+  StageTimer timer(ctx, kStSelectBlocks);
+  SelectArgs s{};
+  s.scores = ctx->J.as<float>();
+  s.stride = Mpad;
+  s.pos = p.pos + q0;
+  s.seq_len = uint32_t(ctx->seq_len);
+  s.num_blocks = uint32_t(num_blocks_of(ctx));
+  s.block_size = ctx->cfg.block_size;
+  s.keep = ctx->cfg.block_budget;
+  s.mode = kSelBlocks;
+  s.tie_break = ctx->cfg.tie_break;
+  s.force_first_last = ctx->cfg.force_first_last;
+  s.forced_in_budget = ctx->cfg.forced_in_budget;
+  s.out_idx = sel;
+  s.out_stride = ctx->cfg.block_budget + 2;
+  s.out_width = ctx->cfg.block_budget + 2;
+  s.out_count = nsel;
+  count_launches(ctx, launch_select(s, uint32_t(nq), s.num_blocks, ctx->stream));
+  return check_launch(ctx, "select_blocks");
+}
+
+// gives `dst` (host or device, may be null) the contents of a device staging array
+int copy_out(hisa_cuda_ctx* ctx, void* dst, const void* src_dev, size_t bytes, bool* need_sync) {
+  if (!dst || dst == src_dev || bytes == 0) return HISA_OK;
+  CU_TRY(ctx, cudaMemcpyAsync(dst, src_dev, bytes, cudaMemcpyDefault, ctx->stream));
+  if (!is_device_ptr(dst)) *need_sync = true;
+  return HISA_OK;
+}
+
+void begin_call(hisa_cuda_ctx* ctx) {
+  ctx->call_launches = 0;
+  ctx->items1 = ctx->items2 = 0;
+  ctx->spans.clear();
+  ctx->events_used = 0;
+  if (ctx->profiling) {
+    if (!ctx->call_beg) {
+      cudaEventCreate(&ctx->call_beg);
+      cudaEventCreate(&ctx->call_end);
+    }
+    cudaEventRecord(ctx->call_beg, ctx->stream);
+  }
+}
+void end_call(hisa_cuda_ctx* ctx) {
+  if (ctx->profiling) cudaEventRecord(ctx->call_end, ctx->stream);
+}
+
+enum Strategy { kDsa = 0, kHisa = 1, kBlockSparse = 2 };
+
+int select_impl(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const float* gates, const uint32_t* positions,
+                uint64_t Q, int check_finite, int32_t* out_idx, uint32_t* out_count, int32_t* out_blocks,
+                uint32_t* out_nblocks, uint32_t* out_cand) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  if (!out_idx && Q) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "out_idx must be non-null");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  begin_call(ctx);
+  if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "selection over an empty key sequence");
+  if (strat != kDsa) HISA_TRY(ensure_pool(ctx));
+  Prepared p;
+  HISA_TRY(prepare_inputs(ctx, queries, gates, positions, Q, check_finite, &p));
+  if (Q == 0) return HISA_OK;
+
+  const hisa_cuda_config& c = ctx->cfg;
+  const uint32_t B = c.block_size, S = c.block_budget + 2, k = c.token_budget;
+  const uint32_t L = uint32_t(ctx->seq_len);
+  const uint32_t M = uint32_t(num_blocks_of(ctx));
+  const uint32_t Mpad = round_up(M, kTileRows);
+  const uint32_t Lpad = round_up(L, kTileRows);
+  const uint32_t out_width = strat == kBlockSparse ? S * B : k;
+  const uint64_t cand_cols = uint64_t(S) * B;
+
+  HISA_TRY(ensure(ctx, ctx->scalars, 64));
+  bool need_sync = false;
+  const bool idx_dev = is_device_ptr(out_idx), cnt_dev = is_device_ptr(out_count);
+  const bool blk_dev = is_device_ptr(out_blocks), nblk_dev = is_device_ptr(out_nblocks);
+  const bool cand_dev = is_device_ptr(out_cand);
+
+  // rows per pass, bounded by the workspace budget
+  uint64_t per_row = 0;
+  if (strat == kDsa) per_row = uint64_t(Lpad) * 4;
+  else per_row = uint64_t(Mpad) * 4 + (strat == kHisa ? cand_cols * 4 : 0) + uint64_t(S) * 12;
+  uint64_t pass_rows = std::max<uint64_t>(ctx->workspace_bytes / std::max<uint64_t>(per_row, 1), 1);
+  const uint64_t chunk_lcm = uint64_t(ctx->chunk_dense) * ctx->chunk_list / std::min(ctx->chunk_dense, ctx->chunk_list);
+  if (pass_rows >= chunk_lcm) pass_rows = pass_rows / chunk_lcm * chunk_lcm;
+  pass_rows = std::min<uint64_t>(pass_rows, Q);
+  pass_rows = std::min<uint64_t>(pass_rows, uint64_t(ctx->chunk_dense) * 4096);
+
+  if (!idx_dev) HISA_TRY(ensure(ctx, ctx->out_idx, size_t(pass_rows) * out_width * 4));
+  if (!cnt_dev) HISA_TRY(ensure(ctx, ctx->out_count, size_t(pass_rows) * 4));
+  if (!cand_dev) HISA_TRY(ensure(ctx, ctx->out_cand, size_t(pass_rows) * 4));
+  if (strat != kDsa) {
+    if (!blk_dev) HISA_TRY(ensure(ctx, ctx->sel, size_t(pass_rows) * S * 4));
+    if (!nblk_dev) HISA_TRY(ensure(ctx, ctx->nsel, size_t(pass_rows) * 4));
+  }
+
+  for (uint64_t q0 = 0; q0 < Q; q0 += pass_rows) {
+    const uint64_t nq = std::min<uint64_t>(pass_rows, Q - q0);
+    int32_t* idx_dst = idx_dev ? out_idx + q0 * out_width : ctx->out_idx.as<int32_t>();
+    uint32_t* cnt_dst = cnt_dev ? out_count + q0 : ctx->out_count.as<uint32_t>();
+    uint32_t* cand_dst = cand_dev ? out_cand + q0 : ctx->out_cand.as<uint32_t>();
+
+    if (strat == kDsa) {
+      // ---- flat indexer: score the whole causal prefix, then top-k (dsa.hpp:29-32) ----
+      const uint32_t ntiles = Lpad / kTileRows;
+      const uint32_t nchunks = uint32_t((nq + ctx->chunk_dense - 1) / ctx->chunk_dense);
+      HISA_TRY(ensure(ctx, ctx->work, size_t(nchunks) * ntiles * sizeof(WorkItem)));
+      HISA_TRY(ensure(ctx, ctx->flat, size_t(nq) * Lpad * 4));
+      uint32_t* sc = ctx->scalars.as<uint32_t>();
+      {
+        StageTimer timer(ctx, kStScoreTokens);
+        count_launches(ctx, launch_build_dense_work(p.pos + q0, uint32_t(nq), ctx->chunk_dense, L, 1, ntiles,
+                                                    ctx->work.as<WorkItem>(), sc, sc + 1, ctx->stream));
+        ScoreJob j{};
+        j.a_op = ctx->key_op.as<__nv_bfloat16>();
+        j.a_rows = L;
+        j.nseg_a = ctx->nseg_k;
+        j.terms = ctx->terms_tok;
+        j.q_op = p.q_op + q0 * kHeads * ctx->nseg_q * kDim;
+        j.nq = nq;
+        j.gates = p.gates + q0 * kHeads;
+        j.out = ctx->flat.as<float>();
+        j.out_stride = Lpad;
+        j.list_mode = false;
+        j.max_items = nchunks * ntiles;
+        ctx->items2 += j.max_items;
+        HISA_TRY(run_scorer(ctx, j));
+      }
+      {
+        StageTimer timer(ctx, kStTopK);
+        SelectArgs s{};
+        s.scores = ctx->flat.as<float>();
+        s.stride = Lpad;
+        s.pos = p.pos + q0;
+        s.seq_len = L;
+        s.num_blocks = M;
+        s.block_size = B;
+        s.keep = k;
+        s.mode = kSelFlat;
+        s.tie_break = c.tie_break;
+        s.out_idx = idx_dst;
+        s.out_stride = out_width;
+        s.out_width = out_width;
+        s.out_count = cnt_dst;
+        s.out_cand = cand_dst;
+        count_launches(ctx, launch_select(s, uint32_t(nq), L, ctx->stream));
+        HISA_TRY(check_launch(ctx, "top-k"));
+      }
+    } else {
+      int32_t* sel = blk_dev ? out_blocks + q0 * S : ctx->sel.as<int32_t>();
+      uint32_t* nsel = nblk_dev ? out_nblocks + q0 : ctx->nsel.as<uint32_t>();
+      // ---- stage 1: block scores + top-m with forced blocks (hisa.hpp:16-28) ----
+      HISA_TRY(run_score_blocks(ctx, p, q0, nq, Mpad));
+      HISA_TRY(run_select_blocks(ctx, p, q0, nq, Mpad, sel, nsel));
+      if (strat == kBlockSparse) {
+        StageTimer timer(ctx, kStTopK);
+        count_launches(ctx, launch_expand_blocks(sel, nsel, S, p.pos + q0, uint32_t(nq), L, B, idx_dst, out_width,
+                                                 out_width, cnt_dst, ctx->stream));
+        HISA_TRY(check_launch(ctx, "expand blocks"));
+      } else {
+        // ---- stage 2: block-major refinement over the selected blocks, then top-k (hisa.hpp:30-45) ----
+        const uint32_t spb = (B + kTileRows - 1) / kTileRows;
+        const uint32_t nchunks = uint32_t((nq + ctx->chunk_list - 1) / ctx->chunk_list);
+        const uint64_t items_cap = uint64_t(nchunks) * std::min<uint64_t>(M, uint64_t(ctx->chunk_list) * S) * spb;
+        HISA_TRY(ensure(ctx, ctx->work, size_t(items_cap) * sizeof(WorkItem)));
+        HISA_TRY(ensure(ctx, ctx->pairs, size_t(nchunks) * ctx->chunk_list * S * sizeof(uint2)));
+        HISA_TRY(ensure(ctx, ctx->cand, size_t(nq) * cand_cols * 4));
+        uint32_t* sc = ctx->scalars.as<uint32_t>();
+        {
+          StageTimer timer(ctx, kStInvert);
+          count_launches(ctx, launch_invert_selection(sel, nsel, S, uint32_t(nq), ctx->chunk_list, M, B, spb,
+                                                      ctx->work.as<WorkItem>(), sc, sc + 1, ctx->pairs.as<uint2>(),
+                                                      ctx->stream));
+          HISA_TRY(check_launch(ctx, "invert selection"));
+        }
+        {
+          StageTimer timer(ctx, kStScoreTokens);
+          ScoreJob j{};
+          j.a_op = ctx->key_op.as<__nv_bfloat16>();
+          j.a_rows = L;
+          j.nseg_a = ctx->nseg_k;
+          j.terms = ctx->terms_tok;
+          j.q_op = p.q_op + q0 * kHeads * ctx->nseg_q * kDim;
+          j.nq = nq;
+          j.gates = p.gates + q0 * kHeads;
+          j.out = ctx->cand.as<float>();
+          j.out_stride = cand_cols;
+          j.list_mode = true;
+          j.pairs = ctx->pairs.as<uint2>();
+          j.max_items = uint32_t(std::min<uint64_t>(items_cap, 0xFFFFFFFFull));
+          ctx->items2 += j.max_items;
+          HISA_TRY(run_scorer(ctx, j));
+        }
+        {
+          StageTimer timer(ctx, kStTopK);
+          SelectArgs s{};
+          s.scores = ctx->cand.as<float>();
+          s.stride = cand_cols;
+          s.pos = p.pos + q0;
+          s.seq_len = L;
+          s.num_blocks = M;
+          s.block_size = B;
+          s.keep = k;
+          s.mode = kSelCand;
+          s.sel = sel;
+          s.nsel = nsel;
+          s.sel_stride = S;
+          s.tie_break = c.tie_break;
+          s.out_idx = idx_dst;
+          s.out_stride = out_width;
+          s.out_width = out_width;
+          s.out_count = cnt_dst;
+          s.out_cand = cand_dst;
+          count_launches(ctx, launch_select(s, uint32_t(nq), uint32_t(std::min<uint64_t>(cand_cols, L)), ctx->stream));
+          HISA_TRY(check_launch(ctx, "top-k"));
+        }
+      }
+      if (!blk_dev) HISA_TRY(copy_out(ctx, out_blocks ? out_blocks + q0 * S : nullptr, sel, size_t(nq) * S * 4, &need_sync));
+      if (!nblk_dev) HISA_TRY(copy_out(ctx, out_nblocks ? out_nblocks + q0 : nullptr, nsel, size_t(nq) * 4, &need_sync));
+    }
+    if (!idx_dev) HISA_TRY(copy_out(ctx, out_idx + q0 * out_width, idx_dst, size_t(nq) * out_width * 4, &need_sync));
+    if (!cnt_dev) HISA_TRY(copy_out(ctx, out_count ? out_count + q0 : nullptr, cnt_dst, size_t(nq) * 4, &need_sync));
+    if (!cand_dev) HISA_TRY(copy_out(ctx, out_cand ? out_cand + q0 : nullptr, cand_dst, size_t(nq) * 4, &need_sync));
+  }
+  end_call(ctx);
+  if (need_sync) CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return HISA_OK;
+}
+
+uint32_t env_u32(const char* name, uint32_t dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  return uint32_t(strtoul(v, nullptr, 10));
+}
+
+}  // namespace
+
+// ==================================================================================================
+// C ABI
+// ==================================================================================================
+extern "C" {
+
+void hisa_cuda_config_init(hisa_cuda_config* cfg, uint32_t block_size, uint32_t block_budget, uint32_t token_budget,
+                           uint32_t num_heads, uint32_t dim, uint32_t dtype) {
+  memset(cfg, 0, sizeof *cfg);
+  cfg->block_size = block_size;
+  cfg->block_budget = block_budget;
+  cfg->token_budget = token_budget;
+  cfg->num_heads = num_heads;
+  cfg->dim = dim;
+  cfg->force_first_last = 1;
+  cfg->forced_in_budget = 0;
+  cfg->tie_break = HISA_TIE_SMALLEST_INDEX;
+  cfg->pool_mode = HISA_POOL_MEAN;
+  cfg->dtype = dtype;
+  cfg->scorer = HISA_SCORER_TENSOR;
+}
+
+int hisa_cuda_config_validate(const hisa_cuda_config* c) {
+  if (!c) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null config");
+  if (c->block_size == 0 || c->block_budget == 0 || c->token_budget == 0 || c->num_heads == 0 || c->dim == 0)
+    return fail(nullptr, HISA_ERR_INFEASIBLE_CONFIG, "config: all integer fields must be strictly positive");
+  const uint64_t cap = uint64_t(c->block_budget) * c->block_size;
+  if (cap < c->token_budget)
+    return fail(nullptr, HISA_ERR_INFEASIBLE_CONFIG,
+                "infeasible config: block budget times block size must satisfy mB >= k (got %u*%u=%llu < %u)",
+                c->block_budget, c->block_size, (unsigned long long)cap, c->token_budget);
+  return HISA_OK;
+}
+
+int hisa_cuda_abi_version(void) { return HISA_CUDA_ABI_VERSION; }
+
+const char* hisa_cuda_status_name(int s) {
+  switch (s) {
+    case HISA_OK: return "OK";
+    case HISA_ERR_INFEASIBLE_CONFIG: return "InfeasibleConfig";
+    case HISA_ERR_CAUSAL_VIOLATION: return "CausalViolation";
+    case HISA_ERR_EMPTY_SEQUENCE: return "EmptySequence";
+    case HISA_ERR_DIMENSION_MISMATCH: return "DimensionMismatch";
+    case HISA_ERR_NON_FINITE: return "NonFiniteValue";
+    case HISA_ERR_SHAPE_MISMATCH: return "ShapeMismatch";
+    case HISA_ERR_EMPTY_SELECTION: return "EmptySelection";
+    case HISA_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+    case HISA_ERR_UNSUPPORTED: return "Unsupported";
+    case HISA_ERR_NO_DEVICE: return "NoDevice";
+    case HISA_ERR_CUDA: return "CudaError";
+    case HISA_ERR_OUT_OF_MEMORY: return "OutOfMemory";
+    default: return "Unknown";
+  }
+}
+
+const char* hisa_cuda_last_error(const hisa_cuda_ctx* ctx) { return ctx ? ctx->err.c_str() : g_global_error.c_str(); }
+
+int hisa_cuda_device_count(int* count) {
+  if (!count) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null count");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+    return fail(nullptr, HISA_ERR_NO_DEVICE, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  *count = n;
+  return HISA_OK;
+}
+
+int hisa_cuda_create(int device, const hisa_cuda_config* cfg, hisa_cuda_ctx** out) {
+  if (!out) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null output pointer");
+  *out = nullptr;
+  HISA_TRY(hisa_cuda_config_validate(cfg));
+  if (cfg->num_heads > uint32_t(kHeads))
+    return fail(nullptr, HISA_ERR_UNSUPPORTED, "num_heads %u > %d is not covered by the sm_100a kernels", cfg->num_heads, kHeads);
+  if (cfg->dim > uint32_t(kDim))
+    return fail(nullptr, HISA_ERR_UNSUPPORTED, "dim %u > %d is not covered by the sm_100a kernels", cfg->dim, kDim);
+  if (cfg->dtype != HISA_DTYPE_F32 && cfg->dtype != HISA_DTYPE_BF16)
+    return fail(nullptr, HISA_ERR_UNSUPPORTED, "unknown dtype %u", cfg->dtype);
+  if (cfg->tie_break > 1 || cfg->pool_mode > 1 || cfg->scorer > 1)
+    return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "config enum field out of range");
+  if (uint64_t(cfg->block_budget) + 2 > 0xFFFFFFull || uint64_t(cfg->block_budget + 2) * cfg->block_size > 0x7FFFFFFFull)
+    return fail(nullptr, HISA_ERR_UNSUPPORTED, "candidate pool (m+2)*B too large");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(nullptr, HISA_ERR_NO_DEVICE, "no CUDA device available (this library has no CPU fallback)");
+  }
+  if (device < 0 || device >= n) return fail(nullptr, HISA_ERR_NO_DEVICE, "device %d out of range (%d devices)", device, n);
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
+    return fail(nullptr, HISA_ERR_NO_DEVICE, "cudaGetDeviceProperties(%d) failed", device);
+  if (prop.major != 10)
+    return fail(nullptr, HISA_ERR_NO_DEVICE, "device %d is sm_%d%d; the kernels are built for sm_100a only", device,
+                prop.major, prop.minor);
+  hisa_cuda_ctx* ctx = new hisa_cuda_ctx();
+  ctx->cfg = *cfg;
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return fail(nullptr, HISA_ERR_CUDA, "could not create a stream on device %d", device);
+  }
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult qres;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qres) != cudaSuccess || !fn) {
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return fail(nullptr, HISA_ERR_CUDA, "cuTensorMapEncodeTiled entry point not available");
+  }
+  ctx->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+
+  const bool bf16 = cfg->dtype == HISA_DTYPE_BF16;
+  if (bf16) {
+    ctx->nseg_k = ctx->nseg_q = 1;
+    ctx->nseg_p = std::min<uint32_t>(std::max<uint32_t>(env_u32("HISA_POOL_SEGS", 2), 1), kMaxSeg);
+    ctx->terms_tok[0] = 1; ctx->terms_tok[1] = ctx->terms_tok[2] = 0;
+    ctx->terms_blk[0] = (1u << ctx->nseg_p) - 1; ctx->terms_blk[1] = ctx->terms_blk[2] = 0;
+  } else {
+    // exact 3-way bf16 split of fp32 operands; keep the six largest cross terms (error ~2^-24 relative)
+    ctx->nseg_k = ctx->nseg_q = ctx->nseg_p = 3;
+    ctx->terms_tok[0] = 0b111; ctx->terms_tok[1] = 0b011; ctx->terms_tok[2] = 0b001;
+    for (int i = 0; i < kMaxSeg; ++i) ctx->terms_blk[i] = ctx->terms_tok[i];
+  }
+  ctx->q_zero_copy = bf16 && cfg->num_heads == uint32_t(kHeads) && cfg->dim == uint32_t(kDim);
+  ctx->chunk_dense = std::max<uint32_t>(env_u32("HISA_CHUNK_DENSE", 256), 4);
+  ctx->chunk_list = std::max<uint32_t>(env_u32("HISA_CHUNK_LIST", 512), 4);
+  ctx->workspace_bytes = uint64_t(std::max<uint32_t>(env_u32("HISA_WORKSPACE_MB", 4096), 16)) << 20;
+  *out = ctx;
+  return HISA_OK;
+}
+
+int hisa_cuda_destroy(hisa_cuda_ctx* ctx) {
+  if (!ctx) return HISA_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (DevBuf* b : {&ctx->key_op, &ctx->key_raw, &ctx->sums, &ctx->counts, &ctx->pooled_op, &ctx->q_raw, &ctx->q_op,
+                    &ctx->gates_raw, &ctx->gates_pad, &ctx->pos, &ctx->J, &ctx->sel, &ctx->nsel, &ctx->work, &ctx->pairs,
+                    &ctx->scalars, &ctx->cand, &ctx->flat, &ctx->out_idx, &ctx->out_count, &ctx->out_cand,
+                    &ctx->generic_scores, &ctx->generic_n, &ctx->export_a, &ctx->export_b, &ctx->flag})
+    release(*b);
+  for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->call_beg) cudaEventDestroy(ctx->call_beg);
+  if (ctx->call_end) cudaEventDestroy(ctx->call_end);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return HISA_OK;
+}
+
+int hisa_cuda_synchronize(hisa_cuda_ctx* ctx) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return HISA_OK;
+}
+
+void* hisa_cuda_stream(hisa_cuda_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int hisa_cuda_host_alloc(void** ptr, size_t bytes) {
+  if (!ptr) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null pointer");
+  cudaError_t e = cudaHostAlloc(ptr, bytes ? bytes : 1, cudaHostAllocDefault);
+  if (e != cudaSuccess) return fail(nullptr, HISA_ERR_OUT_OF_MEMORY, "cudaHostAlloc(%zu): %s", bytes, cudaGetErrorString(e));
+  return HISA_OK;
+}
+int hisa_cuda_host_free(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+  return HISA_OK;
+}
+int hisa_cuda_device_alloc(hisa_cuda_ctx* ctx, void** ptr, size_t bytes) {
+  if (!ctx || !ptr) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "null argument");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  CU_TRY(ctx, cudaMalloc(ptr, bytes ? bytes : 1));
+  return HISA_OK;
+}
+int hisa_cuda_device_free(hisa_cuda_ctx* ctx, void* ptr) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  if (ptr) {
+    CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    CU_TRY(ctx, cudaFree(ptr));
+  }
+  return HISA_OK;
+}
+int hisa_cuda_memcpy(hisa_cuda_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return HISA_OK;
+}
+
+// ---- keys and block summaries ---------------------------------------------------------------------
+
+static int grow_keys(hisa_cuda_ctx* ctx, uint64_t need_tokens) {
+  if (need_tokens <= ctx->key_cap) return HISA_OK;
+  uint64_t cap = std::max<uint64_t>(need_tokens, ctx->key_cap + ctx->key_cap / 2);
+  cap = round_up64(cap, 1024);
+  const size_t row_bytes = size_t(ctx->nseg_k) * kDim * sizeof(__nv_bfloat16);
+  const uint64_t mcap = (cap + ctx->cfg.block_size - 1) / ctx->cfg.block_size + 1;
+  DevBuf nk, ns, nc, np;
+  CU_TRY(ctx, cudaMalloc(&nk.p, cap * row_bytes));
+  CU_TRY(ctx, cudaMalloc(&ns.p, mcap * kDim * sizeof(double)));
+  CU_TRY(ctx, cudaMalloc(&nc.p, mcap * sizeof(uint32_t)));
+  CU_TRY(ctx, cudaMalloc(&np.p, mcap * ctx->nseg_p * kDim * sizeof(__nv_bfloat16)));
+  nk.cap = cap * row_bytes; ns.cap = mcap * kDim * sizeof(double); nc.cap = mcap * sizeof(uint32_t);
+  np.cap = mcap * ctx->nseg_p * kDim * sizeof(__nv_bfloat16);
+  CU_TRY(ctx, cudaMemsetAsync(np.p, 0, np.cap, ctx->stream));
+  if (ctx->seq_len) {
+    const uint64_t M = num_blocks_of(ctx);
+    CU_TRY(ctx, cudaMemcpyAsync(nk.p, ctx->key_op.p, ctx->seq_len * row_bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    CU_TRY(ctx, cudaMemcpyAsync(ns.p, ctx->sums.p, M * kDim * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    CU_TRY(ctx, cudaMemcpyAsync(nc.p, ctx->counts.p, M * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    CU_TRY(ctx, cudaMemcpyAsync(np.p, ctx->pooled_op.p, M * ctx->nseg_p * kDim * sizeof(__nv_bfloat16),
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  release(ctx->key_op); release(ctx->sums); release(ctx->counts); release(ctx->pooled_op);
+  ctx->key_op = nk; ctx->sums = ns; ctx->counts = nc; ctx->pooled_op = np;
+  ctx->key_cap = cap;
+  return HISA_OK;
+}
+
+// converts n keys (host or device, ctx dtype, [n, dim]) into operand rows [first, first+n)
+static int ingest_keys(hisa_cuda_ctx* ctx, const void* keys, uint64_t first, uint64_t n, int check_finite) {
+  const uint32_t d = ctx->cfg.dim, eb = elem_bytes(ctx);
+  const bool bf16 = ctx->cfg.dtype == HISA_DTYPE_BF16;
+  const void* src = keys;
+  const bool direct = bf16 && d == uint32_t(kDim);
+  __nv_bfloat16* dst = ctx->key_op.as<__nv_bfloat16>() + first * ctx->nseg_k * kDim;
+  if (direct) {
+    HISA_TRY(copy_in(ctx, dst, keys, n * d * eb));
+    src = dst;
+  } else if (!is_device_ptr(keys)) {
+    HISA_TRY(ensure(ctx, ctx->key_raw, n * d * eb));
+    HISA_TRY(copy_in(ctx, ctx->key_raw.p, keys, n * d * eb));
+    src = ctx->key_raw.p;
+  }
+  if (check_finite) {
+    HISA_TRY(ensure(ctx, ctx->flag, 16));
+    CU_TRY(ctx, cudaMemsetAsync(ctx->flag.p, 0, 16, ctx->stream));
+    count_launches(ctx, launch_check_finite(src, bf16, n * d, ctx->flag.as<uint32_t>(), ctx->stream));
+    uint32_t bad = 0;
+    HISA_TRY(read_flag(ctx, &bad));
+    if (bad) return fail(ctx, HISA_ERR_NON_FINITE, "inputs: non-finite value in keys");
+  }
+  if (!direct)
+    count_launches(ctx, launch_convert_rows(src, bf16, n, 1, d, ctx->nseg_k, dst, 1, ctx->stream));
+  return check_launch(ctx, "key ingestion");
+}
+
+int hisa_cuda_upload_keys(hisa_cuda_ctx* ctx, const void* keys, uint64_t seq_len, int check_finite) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  if (seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "upload_keys: key matrix has no rows");
+  if (!keys) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "null keys");
+  if (seq_len > 0x7FFFFF00ull) return fail(ctx, HISA_ERR_UNSUPPORTED, "sequence too long");
+  ctx->seq_len = 0;
+  ctx->pooled_tokens = 0;
+  HISA_TRY(grow_keys(ctx, seq_len));
+  HISA_TRY(ingest_keys(ctx, keys, 0, seq_len, check_finite));
+  ctx->seq_len = seq_len;
+  return HISA_OK;
+}
+
+int hisa_cuda_pool_build(hisa_cuda_ctx* ctx) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "build_block_summaries: key matrix has no rows");
+  count_launches(ctx, launch_pool_update(ctx->key_op.as<__nv_bfloat16>(), ctx->nseg_k, 0, ctx->seq_len, ctx->cfg.block_size,
+                                         ctx->cfg.dim, ctx->cfg.pool_mode, ctx->sums.as<double>(), ctx->counts.as<uint32_t>(),
+                                         ctx->pooled_op.as<__nv_bfloat16>(), ctx->nseg_p, ctx->stream));
+  ctx->pooled_tokens = ctx->seq_len;
+  return check_launch(ctx, "pool build");
+}
+
+int hisa_cuda_pool_append(hisa_cuda_ctx* ctx, const void* keys, uint64_t n, uint32_t key_dim) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  if (key_dim != ctx->cfg.dim)
+    return fail(ctx, HISA_ERR_DIMENSION_MISMATCH, "append: key has %u components, cache dimension is %u", key_dim, ctx->cfg.dim);
+  if (n == 0) return HISA_OK;
+  if (!keys) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "null keys");
+  if (ctx->pooled_tokens != ctx->seq_len) HISA_TRY(hisa_cuda_pool_build(ctx));
+  HISA_TRY(grow_keys(ctx, ctx->seq_len + n));
+  HISA_TRY(ingest_keys(ctx, keys, ctx->seq_len, n, 0));
+  count_launches(ctx, launch_pool_update(ctx->key_op.as<__nv_bfloat16>(), ctx->nseg_k, ctx->seq_len, n, ctx->cfg.block_size,
+                                         ctx->cfg.dim, ctx->cfg.pool_mode, ctx->sums.as<double>(), ctx->counts.as<uint32_t>(),
+                                         ctx->pooled_op.as<__nv_bfloat16>(), ctx->nseg_p, ctx->stream));
+  ctx->seq_len += n;
+  ctx->pooled_tokens = ctx->seq_len;
+  return check_launch(ctx, "pool append");
+}
+
+int hisa_cuda_pool_read(hisa_cuda_ctx* ctx, double* sums, uint32_t* counts, double* pooled) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "no block summaries: empty sequence");
+  HISA_TRY(ensure_pool(ctx));
+  const uint32_t M = uint32_t(num_blocks_of(ctx)), d = ctx->cfg.dim;
+  const size_t bytes = size_t(M) * d * sizeof(double);
+  HISA_TRY(ensure(ctx, ctx->export_a, bytes));
+  HISA_TRY(ensure(ctx, ctx->export_b, bytes));
+  count_launches(ctx, launch_pool_export(ctx->sums.as<double>(), ctx->counts.as<uint32_t>(), M, d, ctx->cfg.pool_mode,
+                                         ctx->export_a.as<double>(), ctx->export_b.as<double>(), ctx->stream));
+  HISA_TRY(check_launch(ctx, "pool export"));
+  if (sums) CU_TRY(ctx, cudaMemcpyAsync(sums, ctx->export_a.p, bytes, cudaMemcpyDefault, ctx->stream));
+  if (pooled) CU_TRY(ctx, cudaMemcpyAsync(pooled, ctx->export_b.p, bytes, cudaMemcpyDefault, ctx->stream));
+  if (counts) CU_TRY(ctx, cudaMemcpyAsync(counts, ctx->counts.p, size_t(M) * 4, cudaMemcpyDefault, ctx->stream));
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return HISA_OK;
+}
+
+int hisa_cuda_seq_len(const hisa_cuda_ctx* ctx, uint64_t* seq_len, uint64_t* num_blocks) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  if (seq_len) *seq_len = ctx->seq_len;
+  if (num_blocks) *num_blocks = num_blocks_of(ctx);
+  return HISA_OK;
+}
+
+// ---- batched selection ------------------------------------------------------------------------------
+
+int hisa_cuda_hisa_select(hisa_cuda_ctx* ctx, const void* queries, const float* gates, const uint32_t* positions,
+                          uint64_t num_queries, int check_finite, int32_t* out_idx, uint32_t* out_count,
+                          int32_t* out_blocks, uint32_t* out_nblocks, uint32_t* out_cand) {
+  return select_impl(ctx, kHisa, queries, gates, positions, num_queries, check_finite, out_idx, out_count, out_blocks,
+                     out_nblocks, out_cand);
+}
+
+int hisa_cuda_dsa_select(hisa_cuda_ctx* ctx, const void* queries, const float* gates, const uint32_t* positions,
+                         uint64_t num_queries, int check_finite, int32_t* out_idx, uint32_t* out_count,
+                         uint32_t* out_cand) {
+  return select_impl(ctx, kDsa, queries, gates, positions, num_queries, check_finite, out_idx, out_count, nullptr,
+                     nullptr, out_cand);
+}
+
+int hisa_cuda_block_sparse_select(hisa_cuda_ctx* ctx, const void* queries, const float* gates,
+                                  const uint32_t* positions, uint64_t num_queries, int check_finite, int32_t* out_idx,
+                                  uint32_t* out_count, int32_t* out_blocks, uint32_t* out_nblocks) {
+  return select_impl(ctx, kBlockSparse, queries, gates, positions, num_queries, check_finite, out_idx, out_count,
+                     out_blocks, out_nblocks, nullptr);
+}
+
+// ---- single stages ------------------------------------------------------------------------------------
+
+int hisa_cuda_score_blocks(hisa_cuda_ctx* ctx, const void* queries, const float* gates, const uint32_t* positions,
+                           uint64_t Q, float* out_scores, uint32_t* out_neligible) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  begin_call(ctx);
+  if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "score_blocks: empty block summary cache");
+  HISA_TRY(ensure_pool(ctx));
+  Prepared p;
+  HISA_TRY(prepare_inputs(ctx, queries, gates, positions, Q, 0, &p));
+  if (Q == 0) return HISA_OK;
+  if (Q > uint64_t(ctx->chunk_dense) * 4096) return fail(ctx, HISA_ERR_UNSUPPORTED, "score_blocks: too many rows in one call");
+  HISA_TRY(ensure(ctx, ctx->scalars, 64));
+  const uint32_t M = uint32_t(num_blocks_of(ctx)), Mpad = round_up(M, kTileRows);
+  HISA_TRY(run_score_blocks(ctx, p, 0, Q, Mpad));
+  if (out_scores)
+    CU_TRY(ctx, cudaMemcpy2DAsync(out_scores, size_t(M) * 4, ctx->J.p, size_t(Mpad) * 4, size_t(M) * 4, Q,
+                                  cudaMemcpyDefault, ctx->stream));
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (out_neligible) {
+    // eligibility is pure index arithmetic on the positions (hisa.hpp:18-19)
+    std::vector<uint32_t> pos(Q);
+    CU_TRY(ctx, cudaMemcpy(pos.data(), p.pos, Q * 4, cudaMemcpyDefault));
+    std::vector<uint32_t> ne(Q);
+    for (uint64_t i = 0; i < Q; ++i)
+      ne[i] = std::min<uint32_t>(std::min<uint32_t>(pos[i], uint32_t(ctx->seq_len) - 1) / ctx->cfg.block_size, M - 1) + 1;
+    CU_TRY(ctx, cudaMemcpy(out_neligible, ne.data(), Q * 4, cudaMemcpyDefault));
+  }
+  end_call(ctx);
+  return HISA_OK;
+}
+
+static int generic_select(hisa_cuda_ctx* ctx, bool blocks, const float* scores, uint64_t stride, const uint32_t* n,
+                          uint64_t rows, uint32_t keep, uint32_t out_width, int32_t* out_idx, uint32_t* out_count) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  begin_call(ctx);
+  if (rows == 0) return HISA_OK;
+  if (!scores || !n || !out_idx) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "null argument");
+  if (keep == 0) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "k must be at least 1");
+  const float* s_dev = scores;
+  if (!is_device_ptr(scores)) {
+    HISA_TRY(ensure(ctx, ctx->generic_scores, rows * stride * 4));
+    HISA_TRY(copy_in(ctx, ctx->generic_scores.p, scores, rows * stride * 4));
+    s_dev = ctx->generic_scores.as<float>();
+  }
+  std::vector<uint32_t> n_host(rows);
+  CU_TRY(ctx, cudaMemcpyAsync(n_host.data(), n, rows * 4, cudaMemcpyDefault, ctx->stream));
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  uint32_t n_cap = 1;
+  for (uint64_t i = 0; i < rows; ++i) {
+    if (n_host[i] > stride) return fail(ctx, HISA_ERR_SHAPE_MISMATCH, "row %llu has more candidates than the score stride", (unsigned long long)i);
+    if (blocks && n_host[i] == 0) return fail(ctx, HISA_ERR_EMPTY_SELECTION, "select_blocks: no eligible block in row %llu", (unsigned long long)i);
+    n_cap = std::max(n_cap, n_host[i]);
+  }
+  HISA_TRY(ensure(ctx, ctx->generic_n, rows * 4));
+  HISA_TRY(copy_in(ctx, ctx->generic_n.p, n_host.data(), rows * 4));
+  const bool idx_dev = is_device_ptr(out_idx), cnt_dev = is_device_ptr(out_count);
+  if (!idx_dev) HISA_TRY(ensure(ctx, ctx->out_idx, rows * out_width * 4));
+  if (!cnt_dev) HISA_TRY(ensure(ctx, ctx->out_count, rows * 4));
+  SelectArgs s{};
+  s.scores = s_dev;
+  s.stride = stride;
+  s.n_in = ctx->generic_n.as<uint32_t>();
+  s.seq_len = 0xFFFFFFFFu;
+  s.block_size = ctx->cfg.block_size;
+  s.keep = keep;
+  s.mode = blocks ? kSelBlocksGeneric : kSelGeneric;
+  s.tie_break = ctx->cfg.tie_break;
+  s.force_first_last = ctx->cfg.force_first_last;
+  s.forced_in_budget = ctx->cfg.forced_in_budget;
+  s.out_idx = idx_dev ? out_idx : ctx->out_idx.as<int32_t>();
+  s.out_stride = out_width;
+  s.out_width = out_width;
+  s.out_count = cnt_dev ? out_count : ctx->out_count.as<uint32_t>();
+  count_launches(ctx, launch_select(s, uint32_t(rows), n_cap, ctx->stream));
+  HISA_TRY(check_launch(ctx, "select"));
+  bool need_sync = true;
+  if (!idx_dev) HISA_TRY(copy_out(ctx, out_idx, s.out_idx, rows * out_width * 4, &need_sync));
+  if (!cnt_dev) HISA_TRY(copy_out(ctx, out_count, s.out_count, rows * 4, &need_sync));
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  end_call(ctx);
+  return HISA_OK;
+}
+
+int hisa_cuda_select_blocks(hisa_cuda_ctx* ctx, const float* scores, uint64_t score_stride, const uint32_t* neligible,
+                            uint64_t num_queries, int32_t* out_blocks, uint32_t* out_nblocks) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  return generic_select(ctx, true, scores, score_stride, neligible, num_queries, ctx->cfg.block_budget,
+                        ctx->cfg.block_budget + 2, out_blocks, out_nblocks);
+}
+
+int hisa_cuda_top_k(hisa_cuda_ctx* ctx, const float* scores, uint64_t score_stride, const uint32_t* n, uint64_t num_rows,
+                    uint32_t k, int32_t* out_idx, uint32_t* out_count) {
+  return generic_select(ctx, false, scores, score_stride, n, num_rows, k, k, out_idx, out_count);
+}
+
+int hisa_cuda_score_tokens(hisa_cuda_ctx* ctx, const void* queries, const float* gates, const uint32_t* positions,
+                           uint64_t Q, float* out_scores, uint64_t out_stride) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  begin_call(ctx);
+  if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "score_tokens: empty key sequence");
+  Prepared p;
+  HISA_TRY(prepare_inputs(ctx, queries, gates, positions, Q, 0, &p));
+  if (Q == 0) return HISA_OK;
+  if (!out_scores) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "null out_scores");
+  const uint32_t L = uint32_t(ctx->seq_len), Lpad = round_up(L, kTileRows);
+  if (out_stride < Lpad) return fail(ctx, HISA_ERR_SHAPE_MISMATCH, "score_tokens: out_stride %llu < %u", (unsigned long long)out_stride, Lpad);
+  if (Q > uint64_t(ctx->chunk_dense) * 4096) return fail(ctx, HISA_ERR_UNSUPPORTED, "score_tokens: too many rows in one call");
+  HISA_TRY(ensure(ctx, ctx->scalars, 64));
+  const uint32_t ntiles = Lpad / kTileRows;
+  const uint32_t nchunks = uint32_t((Q + ctx->chunk_dense - 1) / ctx->chunk_dense);
+  HISA_TRY(ensure(ctx, ctx->work, size_t(nchunks) * ntiles * sizeof(WorkItem)));
+  const bool out_dev = is_device_ptr(out_scores);
+  if (!out_dev) HISA_TRY(ensure(ctx, ctx->flat, size_t(Q) * Lpad * 4));
+  uint32_t* sc = ctx->scalars.as<uint32_t>();
+  StageTimer* timer = new StageTimer(ctx, kStScoreTokens);
+  count_launches(ctx, launch_build_dense_work(p.pos, uint32_t(Q), ctx->chunk_dense, L, 1, ntiles, ctx->work.as<WorkItem>(),
+                                              sc, sc + 1, ctx->stream));
+  ScoreJob j{};
+  j.a_op = ctx->key_op.as<__nv_bfloat16>();
+  j.a_rows = L;
+  j.nseg_a = ctx->nseg_k;
+  j.terms = ctx->terms_tok;
+  j.q_op = p.q_op;
+  j.nq = Q;
+  j.gates = p.gates;
+  j.out = out_dev ? out_scores : ctx->flat.as<float>();
+  j.out_stride = out_dev ? out_stride : Lpad;
+  j.list_mode = false;
+  j.max_items = nchunks * ntiles;
+  int rc = run_scorer(ctx, j);
+  delete timer;
+  HISA_TRY(rc);
+  if (!out_dev)
+    CU_TRY(ctx, cudaMemcpy2DAsync(out_scores, out_stride * 4, ctx->flat.p, size_t(Lpad) * 4, size_t(Lpad) * 4, Q,
+                                  cudaMemcpyDefault, ctx->stream));
+  end_call(ctx);
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return HISA_OK;
+}
+
+// ---- instrumentation -------------------------------------------------------------------------------------
+
+int hisa_cuda_set_profiling(hisa_cuda_ctx* ctx, int enable) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  ctx->profiling = enable != 0;
+  return HISA_OK;
+}
+
+int hisa_cuda_last_stage_times(hisa_cuda_ctx* ctx, hisa_cuda_stage_times* out) {
+  if (!ctx || !out) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "null argument");
+  memset(out, 0, sizeof *out);
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  float* slot[kNumStages] = {&out->prepare_ms,  &out->score_blocks_ms, &out->select_blocks_ms,
+                             &out->invert_ms,   &out->score_tokens_ms, &out->top_k_ms};
+  for (const StageSpan& s : ctx->spans) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, s.beg, s.end) == cudaSuccess) *slot[s.stage] += ms;
+  }
+  if (ctx->profiling && ctx->call_beg && cudaEventQuery(ctx->call_end) == cudaSuccess)
+    cudaEventElapsedTime(&out->total_ms, ctx->call_beg, ctx->call_end);
+  cudaGetLastError();
+  out->launches = ctx->call_launches;
+  out->work_items_stage1 = ctx->items1;
+  out->work_items_stage2 = ctx->items2;
+  return HISA_OK;
+}
+
+int hisa_cuda_launch_count(const hisa_cuda_ctx* ctx, uint64_t* launches) {
+  if (!ctx || !launches) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null argument");
+  *launches = ctx->launches;
+  return HISA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,125 @@
+// Internal device-side contracts shared by the kernels and the context (not part of the C ABI).
+//
+// Operand layout in HBM:
+//   key operand   bf16 [L_cap,  nseg_k * 128]   row s = key s, split into nseg_k bf16 segments, d padded to 128
+//   pooled operand bf16 [M_cap, nseg_p * 128]   row b = pooled key of block b (hi | lo [| lo2] split of the f32 mean)
+//   query operand bf16 [Q * 64, nseg_q * 128]   row t*64+j = head j of query t (heads padded to 64 with zeros)
+//   gates         f32  [Q, 64]                  padded with zeros
+// A "tile" is 128 consecutive operand rows (the tcgen05 M extent); a "group" is 4 queries x 64 heads
+// (the tcgen05 N extent, 256 columns of TMEM).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hisa_dev {
+
+constexpr int kTileRows = 128;  // operand rows per tile (UMMA M)
+constexpr int kHeads = 64;      // heads per query in the operand (padded)
+constexpr int kDim = 128;       // elements per operand segment (padded d)
+constexpr int kGroupQ = 4;      // queries per MMA group (UMMA N = 256)
+constexpr int kMaxSeg = 3;
+
+// One unit of scorer work: one operand tile against `count` queries.
+//   dense mode: queries are rows first .. first+count-1, results go to out[row, tile*128 + lane]
+//   list  mode: queries are pairs[first + i] = {row, col}, results go to out[row, col + (tile % spb)*128 + lane]
+struct WorkItem {
+  uint32_t tile;
+  uint32_t first;
+  uint32_t count;
+  uint32_t reserved;
+};
+
+struct ScoreArgs {
+  const WorkItem* work;
+  const uint32_t* work_count;  // device scalar: number of valid items in `work`
+  uint32_t* work_cursor;       // device scalar, zeroed before launch: dynamic scheduler
+  const uint2* pairs;          // list mode
+  const float* gates;          // [Q, 64]
+  float* out;
+  uint64_t out_stride;         // floats per output row
+  uint32_t list_mode;
+  uint32_t segs_per_block;     // list mode: tiles per key block = ceil(B / 128); dense: 1
+  uint32_t block_rows;         // list mode: B; dense: 128
+  uint32_t nseg_a, nseg_b;     // operand segments of the tile (A) and query (B) operands
+  uint32_t terms[kMaxSeg];     // terms[ib] = bit mask of A segments multiplied with B segment ib
+  uint32_t a_rows;             // rows that exist in the A operand (rows beyond read as zero)
+};
+
+// tile -> first operand row and number of meaningful rows
+__host__ __device__ inline uint32_t tile_row0(const ScoreArgs& a, uint32_t tile) {
+  return (tile / a.segs_per_block) * a.block_rows + (tile % a.segs_per_block) * kTileRows;
+}
+__host__ __device__ inline uint32_t tile_valid_rows(const ScoreArgs& a, uint32_t tile) {
+  const uint32_t off = (tile % a.segs_per_block) * kTileRows;
+  const uint32_t left = a.block_rows - off;
+  return left < (uint32_t)kTileRows ? left : (uint32_t)kTileRows;
+}
+
+enum SelectMode : uint32_t {
+  kSelFlat = 0,       // n = t_eff + 1 candidates at positions 0..n-1                  (dsa top-k)
+  kSelBlocks = 1,     // n = t_eff / B + 1 block scores, forced first/last, output = block ids (select_blocks)
+  kSelCand = 2,       // candidates are the tokens of the row's selected blocks        (hisa top-k)
+  kSelGeneric = 3,    // n = n_in[row] candidates at positions 0..n-1                  (top_k_tokens)
+  kSelBlocksGeneric = 4  // like kSelBlocks with n = n_in[row]                         (select_blocks)
+};
+
+struct SelectArgs {
+  const float* scores;
+  uint64_t stride;
+  const uint32_t* pos;   // [rows] query positions (modes 0,1,2)
+  const uint32_t* n_in;  // [rows] candidate counts (modes 3,4)
+  uint32_t seq_len, num_blocks, block_size, keep;  // keep = k (tokens) or m (blocks)
+  uint32_t mode;
+  const int32_t* sel;  // mode 2: [rows, sel_stride] selected blocks ascending
+  const uint32_t* nsel;
+  uint32_t sel_stride;
+  uint32_t tie_break, force_first_last, forced_in_budget;
+  int32_t* out_idx;  // [rows, out_stride], -1 padded
+  uint64_t out_stride;
+  uint32_t out_width;  // entries to write per row (k, or m+2 for block modes)
+  uint32_t* out_count;
+  uint32_t* out_cand;
+};
+
+// ---- launchers (each returns the number of kernels it launched) ---------------------------------
+int launch_score_tc(const ScoreArgs& args, const CUtensorMap& map_a, const CUtensorMap& map_b, int num_sms,
+                    cudaStream_t stream);
+int launch_score_simt(const ScoreArgs& args, const __nv_bfloat16* a_op, const __nv_bfloat16* q_op,
+                      uint32_t max_items, cudaStream_t stream);
+size_t score_tc_smem_bytes(uint32_t nseg_a);
+
+int launch_select(const SelectArgs& args, uint32_t rows, uint32_t n_cap, cudaStream_t stream);
+
+// dense work list: chunk-major list of (tile, chunk) items for rows [0, nq) in chunks of `chunk` queries;
+// tile needed iff tile*128 <= min(max position in chunk, seq_len-1) / unit_div.
+int launch_build_dense_work(const uint32_t* pos, uint32_t nq, uint32_t chunk, uint32_t seq_len, uint32_t unit_div,
+                            uint32_t ntiles, WorkItem* work, uint32_t* work_count, uint32_t* work_cursor,
+                            cudaStream_t stream);
+// list work: per chunk of queries, the per-block lists of (row, slot*B) pairs and one item per (block, seg)
+int launch_invert_selection(const int32_t* sel, const uint32_t* nsel, uint32_t sel_stride, uint32_t nq,
+                            uint32_t chunk, uint32_t num_blocks, uint32_t block_size, uint32_t segs_per_block,
+                            WorkItem* work, uint32_t* work_count, uint32_t* work_cursor, uint2* pairs,
+                            cudaStream_t stream);
+// block-sparse output: tokens of the selected blocks clipped to <= t_eff
+int launch_expand_blocks(const int32_t* sel, const uint32_t* nsel, uint32_t sel_stride, const uint32_t* pos,
+                         uint32_t nq, uint32_t seq_len, uint32_t block_size, int32_t* out_idx, uint64_t out_stride,
+                         uint32_t out_width, uint32_t* out_count, cudaStream_t stream);
+
+// operand preparation
+int launch_convert_rows(const void* src, uint32_t src_is_bf16, uint64_t rows, uint32_t src_heads_or_1,
+                        uint32_t src_dim, uint32_t nseg, __nv_bfloat16* dst, uint32_t dst_heads_or_1,
+                        cudaStream_t stream);
+int launch_pad_gates(const float* src, uint64_t rows, uint32_t heads, float* dst, cudaStream_t stream);
+int launch_check_finite(const void* src, uint32_t is_bf16, uint64_t n, uint32_t* flag, cudaStream_t stream);
+int launch_check_positions(const uint32_t* pos, uint64_t n, uint32_t seq_len, uint32_t* flag, cudaStream_t stream);
+// block summaries over tokens [first, first+n): double sums, counts, pooled operand (nseg_p segments)
+int launch_pool_update(const __nv_bfloat16* key_op, uint32_t nseg_k, uint64_t first, uint64_t n, uint32_t block_size,
+                       uint32_t dim, uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op,
+                       uint32_t nseg_p, cudaStream_t stream);
+int launch_pool_export(const double* sums, const uint32_t* counts, uint32_t num_blocks, uint32_t dim,
+                       uint32_t pool_max, double* out_sums, double* out_pooled, cudaStream_t stream);
+
+}  // namespace hisa_dev

@@ -1,0 +1,186 @@
+// Operand preparation and block mean-pooling kernels (north-star kernel 1).
+//
+// Reference semantics reproduced: hisa::BlockSummaryCache::append / pooled and build_block_summaries
+// (proj/core/include/hisa/block_summary.hpp:23-59): per-block sums accumulated in
+// DOUBLE in position order, counts, pooled(b) = sum / count, last block partial. The batch build and the
+// incremental tail update run the same per-column sequential double accumulation, so they agree bit for
+// bit with each other and with a CPU loop in the same order.
+#include "kernels.cuh"
+
+namespace hisa_dev {
+
+namespace {
+
+__device__ __forceinline__ void split_bf16(float x, int nseg, __nv_bfloat16* parts) {
+  // exact multi-term bf16 expansion of an fp32 value: x == parts[0] + parts[1] + parts[2] for nseg = 3
+  float r = x;
+#pragma unroll
+  for (int s = 0; s < kMaxSeg; ++s) {
+    if (s < nseg) {
+      parts[s] = __float2bfloat16_rn(r);
+      r -= __bfloat162float(parts[s]);
+    }
+  }
+}
+
+// dst row (o*dst_heads + h) <- src row (o*src_heads + h) for h < src_heads, zero rows otherwise;
+// columns >= src_dim are zero. One thread per (dst row, 8-column group).
+__global__ void convert_rows_kernel(const void* __restrict__ src, uint32_t src_is_bf16, uint64_t outer,
+                                    uint32_t src_heads, uint32_t src_dim, uint32_t nseg,
+                                    __nv_bfloat16* __restrict__ dst, uint32_t dst_heads) {
+  const uint64_t gid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t total = outer * dst_heads * (kDim / 8);
+  if (gid >= total) return;
+  const uint32_t cg = uint32_t(gid % (kDim / 8));
+  const uint64_t drow = gid / (kDim / 8);
+  const uint32_t h = uint32_t(drow % dst_heads);
+  const uint64_t o = drow / dst_heads;
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = 0.f;
+  if (h < src_heads) {
+    const uint64_t srow = o * src_heads + h;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t c = cg * 8 + i;
+      if (c < src_dim) {
+        v[i] = src_is_bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(src)[srow * src_dim + c])
+                           : static_cast<const float*>(src)[srow * src_dim + c];
+      }
+    }
+  }
+  __align__(16) __nv_bfloat16 seg[kMaxSeg][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    __nv_bfloat16 parts[kMaxSeg];
+    split_bf16(v[i], int(nseg), parts);
+#pragma unroll
+    for (int s = 0; s < kMaxSeg; ++s)
+      if (s < int(nseg)) seg[s][i] = parts[s];
+  }
+  __nv_bfloat16* drow_ptr = dst + drow * (uint64_t(nseg) * kDim);
+#pragma unroll
+  for (int s = 0; s < kMaxSeg; ++s)
+    if (s < int(nseg)) *reinterpret_cast<uint4*>(drow_ptr + s * kDim + cg * 8) = *reinterpret_cast<const uint4*>(seg[s]);
+}
+
+__global__ void pad_gates_kernel(const float* __restrict__ src, uint64_t rows, uint32_t heads,
+                                 float* __restrict__ dst) {
+  const uint64_t gid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= rows * kHeads) return;
+  const uint32_t h = uint32_t(gid % kHeads);
+  const uint64_t r = gid / kHeads;
+  dst[gid] = h < heads ? src[r * heads + h] : 0.f;
+}
+
+__global__ void check_finite_kernel(const void* __restrict__ src, uint32_t is_bf16, uint64_t n,
+                                    uint32_t* __restrict__ flag) {
+  bool bad = false;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const float v = is_bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(src)[i])
+                            : static_cast<const float*>(src)[i];
+    bad |= !isfinite(v);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+__global__ void check_positions_kernel(const uint32_t* __restrict__ pos, uint64_t n, uint32_t seq_len,
+                                       uint32_t* __restrict__ flag) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && pos[i] > seq_len) atomicOr(flag, 1u);
+}
+
+// One CTA per touched block, one thread per operand column. Sequential (position-order) accumulation.
+__global__ void __launch_bounds__(kDim)
+pool_update_kernel(const __nv_bfloat16* __restrict__ key_op, uint32_t nseg_k, uint64_t first, uint64_t n,
+                   uint32_t block_size, uint32_t pool_max, double* __restrict__ sums,
+                   uint32_t* __restrict__ counts, __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p) {
+  const uint64_t b = first / block_size + blockIdx.x;
+  const uint32_t c = threadIdx.x;
+  const uint64_t blk_lo = b * block_size;
+  const uint64_t s_lo = first > blk_lo ? first : blk_lo;
+  const uint64_t blk_hi = blk_lo + block_size;
+  const uint64_t s_hi = (first + n) < blk_hi ? (first + n) : blk_hi;
+  const bool fresh = (s_lo == blk_lo);
+  double acc = fresh ? 0.0 : sums[b * kDim + c];
+  const uint64_t row_elems = uint64_t(nseg_k) * kDim;
+  for (uint64_t s = s_lo; s < s_hi; ++s) {
+    const __nv_bfloat16* row = key_op + s * row_elems + c;
+    double v = 0.0;
+    for (uint32_t g = 0; g < nseg_k; ++g) v += double(__bfloat162float(row[g * kDim]));
+    if (pool_max) acc = (fresh && s == s_lo) ? v : (v > acc ? v : acc);
+    else acc += v;
+  }
+  sums[b * kDim + c] = acc;
+  const uint32_t cnt = uint32_t(s_hi - blk_lo);
+  if (c == 0) counts[b] = cnt;
+  const double p = pool_max ? acc : acc / double(cnt);
+  __nv_bfloat16 parts[kMaxSeg];
+  split_bf16(float(p), int(nseg_p), parts);
+  for (uint32_t g = 0; g < nseg_p; ++g) pooled_op[b * (uint64_t(nseg_p) * kDim) + g * kDim + c] = parts[g];
+}
+
+__global__ void pool_export_kernel(const double* __restrict__ sums, const uint32_t* __restrict__ counts,
+                                   uint32_t num_blocks, uint32_t dim, uint32_t pool_max,
+                                   double* __restrict__ out_sums, double* __restrict__ out_pooled) {
+  const uint64_t gid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= uint64_t(num_blocks) * dim) return;
+  const uint32_t c = uint32_t(gid % dim);
+  const uint32_t b = uint32_t(gid / dim);
+  const double s = sums[uint64_t(b) * kDim + c];
+  if (out_sums) out_sums[gid] = s;
+  if (out_pooled) out_pooled[gid] = pool_max ? s : s / double(counts[b]);
+}
+
+inline uint32_t blocks_for(uint64_t n, uint32_t threads) { return uint32_t((n + threads - 1) / threads); }
+
+}  // namespace
+
+int launch_convert_rows(const void* src, uint32_t src_is_bf16, uint64_t outer, uint32_t src_heads, uint32_t src_dim,
+                        uint32_t nseg, __nv_bfloat16* dst, uint32_t dst_heads, cudaStream_t stream) {
+  const uint64_t total = outer * dst_heads * (kDim / 8);
+  if (total == 0) return 0;
+  convert_rows_kernel<<<blocks_for(total, 256), 256, 0, stream>>>(src, src_is_bf16, outer, src_heads, src_dim, nseg,
+                                                                  dst, dst_heads);
+  return 1;
+}
+
+int launch_pad_gates(const float* src, uint64_t rows, uint32_t heads, float* dst, cudaStream_t stream) {
+  if (rows == 0) return 0;
+  pad_gates_kernel<<<blocks_for(rows * kHeads, 256), 256, 0, stream>>>(src, rows, heads, dst);
+  return 1;
+}
+
+int launch_check_finite(const void* src, uint32_t is_bf16, uint64_t n, uint32_t* flag, cudaStream_t stream) {
+  if (n == 0) return 0;
+  const uint32_t grid = uint32_t(n / 256 + 1 < 148 * 16 ? n / 256 + 1 : 148 * 16);
+  check_finite_kernel<<<grid, 256, 0, stream>>>(src, is_bf16, n, flag);
+  return 1;
+}
+
+int launch_check_positions(const uint32_t* pos, uint64_t n, uint32_t seq_len, uint32_t* flag, cudaStream_t stream) {
+  if (n == 0) return 0;
+  check_positions_kernel<<<blocks_for(n, 256), 256, 0, stream>>>(pos, n, seq_len, flag);
+  return 1;
+}
+
+int launch_pool_update(const __nv_bfloat16* key_op, uint32_t nseg_k, uint64_t first, uint64_t n, uint32_t block_size,
+                       uint32_t /*dim*/, uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op,
+                       uint32_t nseg_p, cudaStream_t stream) {
+  if (n == 0) return 0;
+  const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
+  pool_update_kernel<<<uint32_t(b1 - b0 + 1), kDim, 0, stream>>>(key_op, nseg_k, first, n, block_size, pool_max, sums,
+                                                                 counts, pooled_op, nseg_p);
+  return 1;
+}
+
+int launch_pool_export(const double* sums, const uint32_t* counts, uint32_t num_blocks, uint32_t dim, uint32_t pool_max,
+                       double* out_sums, double* out_pooled, cudaStream_t stream) {
+  const uint64_t total = uint64_t(num_blocks) * dim;
+  if (total == 0) return 0;
+  pool_export_kernel<<<blocks_for(total, 256), 256, 0, stream>>>(sums, counts, num_blocks, dim, pool_max, out_sums,
+                                                                 out_pooled);
+  return 1;
+}
+
+}  // namespace hisa_dev

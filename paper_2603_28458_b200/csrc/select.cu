@@ -1,0 +1,425 @@
+// Selection kernels (north-star kernels 3 and 5) and the work-list builders that feed the scorer.
+//
+// select_rows_kernel reproduces hisa::top_k_tokens (proj/core/include/hisa/dsa.hpp:22-27)
+// and hisa::select_blocks (hisa/hisa.hpp:23-28) on fp32 scores:
+//   total order = (score descending, then position ascending for SmallestIndex / descending for
+//   LargestIndex), keep the first `keep` entries of that order, emit them in ascending position order;
+//   +0 and -0 compare equal. For blocks, the first eligible block and the block containing the query are
+//   added on top (force_first_last), or placed first inside the budget (forced_in_budget).
+// Method: scores -> order-preserving u32 keys in shared memory; the keep-th largest key T is found by a
+// range-adaptive radix select (11-bit digits over [min,max], so fp32 scores that share sign/exponent do
+// not pile into one bin); then ONE ordered compaction in position order emits keys > T plus the required
+// number of keys == T picked from the front (SmallestIndex) or the back (LargestIndex). That yields the
+// reference's tie-break and its ascending output without sorting.
+//
+// candidate_union (hisa/hisa.hpp:30-33) never materialises: stage-2 candidates are addressed as
+// (slot, offset) inside the row's selected-block list and mapped to token positions on output.
+#include "kernels.cuh"
+
+namespace hisa_dev {
+
+namespace {
+
+constexpr int kBins = 2048;
+constexpr int kBinBits = 11;
+
+__device__ __forceinline__ uint32_t score_key(float f) {
+  uint32_t b = __float_as_uint(f);
+  if (b == 0x80000000u) b = 0u;  // -0 == +0
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// exclusive prefix sum over the block; `total` receives the block sum. scratch: >= 33 words.
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_scan_excl(uint32_t v, uint32_t* scratch, uint32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  __syncthreads();  // scratch reuse across calls
+  if (lane == 31) scratch[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int NW = THREADS / 32;
+    uint32_t w = lane < NW ? scratch[lane] : 0u;
+    uint32_t winc = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, winc, o);
+      if (lane >= o) winc += y;
+    }
+    if (lane < NW) scratch[lane] = winc - w;
+    if (lane == NW - 1) scratch[32] = winc;
+  }
+  __syncthreads();
+  total = scratch[32];
+  return scratch[warp] + inc - v;
+}
+
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_reduce_min(uint32_t v, uint32_t* scratch) {
+  v = __reduce_min_sync(0xffffffffu, v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+  __syncthreads();
+  uint32_t r = scratch[0];
+  for (int w = 1; w < THREADS / 32; ++w) r = min(r, scratch[w]);
+  return r;
+}
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_reduce_max(uint32_t v, uint32_t* scratch) {
+  v = __reduce_max_sync(0xffffffffu, v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+  __syncthreads();
+  uint32_t r = scratch[0];
+  for (int w = 1; w < THREADS / 32; ++w) r = max(r, scratch[w]);
+  return r;
+}
+
+template <int THREADS, bool SMEM_KEYS>
+__global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
+  extern __shared__ __align__(16) uint32_t smem_u[];
+  uint32_t* hist = smem_u;               // [kBins]
+  uint32_t* scratch = smem_u + kBins;    // [64]
+  uint32_t* skey = smem_u + kBins + 64;  // [n_cap] when SMEM_KEYS
+
+  const uint32_t row = blockIdx.x;
+  const uint32_t tid = threadIdx.x;
+  const bool block_mode = (a.mode == kSelBlocks || a.mode == kSelBlocksGeneric);
+  const uint32_t B = a.block_size;
+
+  // ---- how many candidates does this row have, and where do they live -------------------------
+  uint32_t n = 0;
+  const int32_t* sel_row = nullptr;
+  if (a.mode == kSelFlat) {
+    const uint32_t t = min(a.pos[row], a.seq_len - 1);
+    n = t + 1;
+  } else if (a.mode == kSelBlocks) {
+    const uint32_t t = min(a.pos[row], a.seq_len - 1);
+    n = min(t / B, a.num_blocks - 1) + 1;
+  } else if (a.mode == kSelCand) {
+    const uint32_t t = min(a.pos[row], a.seq_len - 1);
+    const uint32_t ns = a.nsel[row];
+    sel_row = a.sel + uint64_t(row) * a.sel_stride;
+    const uint32_t lastb = uint32_t(sel_row[ns - 1]);
+    n = (ns - 1) * B + min(B, t - lastb * B + 1);
+  } else {
+    n = a.n_in[row];
+  }
+  const float* srow = a.scores + uint64_t(row) * a.stride;
+  int32_t* orow = a.out_idx + uint64_t(row) * a.out_stride;
+  const uint32_t keep = a.keep;
+  const bool forced = block_mode && a.force_first_last && n > 0;
+
+  auto position_of = [&](uint32_t i) -> int32_t {
+    if (a.mode == kSelCand) return sel_row[i / B] * int32_t(B) + int32_t(i % B);
+    return int32_t(i);
+  };
+
+  if (a.out_cand && tid == 0) a.out_cand[row] = n;
+
+  // ---- everything fits: dense regime ------------------------------------
+  if (n <= keep) {
+    for (uint32_t i = tid; i < a.out_width; i += THREADS) orow[i] = i < n ? position_of(i) : -1;
+    if (a.out_count && tid == 0) a.out_count[row] = n;
+    return;
+  }
+
+  auto raw_key = [&](uint32_t i) -> uint32_t {
+    uint32_t key = score_key(srow[i]);
+    if (forced && a.forced_in_budget && (i == 0 || i == n - 1)) key = 0xFFFFFFFFu;
+    return key;
+  };
+  auto key_at = [&](uint32_t i) -> uint32_t {
+    if constexpr (SMEM_KEYS) return skey[i];
+    else return raw_key(i);
+  };
+
+  // ---- keys, min, max ---------------------------------------------------------------------------
+  uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+  for (uint32_t i = tid; i < n; i += THREADS) {
+    const uint32_t key = raw_key(i);
+    if constexpr (SMEM_KEYS) skey[i] = key;
+    kmin = min(kmin, key);
+    kmax = max(kmax, key);
+  }
+  uint32_t lo = block_reduce_min<THREADS>(kmin, scratch);
+  uint32_t hi = block_reduce_max<THREADS>(kmax, scratch);
+  __syncthreads();
+
+  // ---- range-adaptive radix select of the keep-th largest key ------------------------------------
+  uint32_t kk = keep;  // still to take from [lo, hi]
+  while (lo != hi) {
+    const uint32_t range = hi - lo;
+    const uint32_t nb = 32 - __clz(range);
+    const uint32_t shift = nb > kBinBits ? nb - kBinBits : 0u;
+    for (uint32_t i = tid; i < kBins; i += THREADS) hist[i] = 0u;
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += THREADS) {
+      const uint32_t key = key_at(i);
+      if (key >= lo && key <= hi) atomicAdd(&hist[(key - lo) >> shift], 1u);
+    }
+    __syncthreads();
+    constexpr int BPT = kBins / THREADS;
+    uint32_t loc = 0;
+#pragma unroll
+    for (int j = 0; j < BPT; ++j) loc += hist[tid * BPT + j];
+    uint32_t total;
+    const uint32_t before = block_scan_excl<THREADS>(loc, scratch, total);
+    const uint32_t above = total - before - loc;  // keys in bins owned by higher threads
+    if (above < kk && kk <= above + loc) {
+      uint32_t c = above;
+      int j = BPT - 1;
+      for (; j > 0; --j) {
+        const uint32_t h = hist[tid * BPT + j];
+        if (c + h >= kk) break;
+        c += h;
+      }
+      scratch[40] = tid * BPT + j;
+      scratch[41] = c;
+    }
+    __syncthreads();
+    const uint32_t bin = scratch[40];
+    kk -= scratch[41];
+    lo = lo + (bin << shift);
+    const uint32_t width = (shift == 0) ? 0u : ((1u << shift) - 1u);
+    hi = min(hi, lo + width);
+    __syncthreads();
+  }
+  const uint32_t T = lo;
+  const uint32_t need = kk;  // ties (key == T) to take
+
+  // ---- ordered compaction over blocked segments ---------------------------------------------------
+  const uint32_t ipt = ((n + THREADS - 1) / THREADS) | 1u;  // odd: conflict-free strided smem walks
+  const uint32_t s0 = min(n, tid * ipt), s1 = min(n, s0 + ipt);
+  uint32_t cG = 0, cE = 0;
+  for (uint32_t i = s0; i < s1; ++i) {
+    const uint32_t key = key_at(i);
+    cG += key > T;
+    cE += key == T;
+  }
+  uint32_t totG, totE;
+  const uint32_t gBefore = block_scan_excl<THREADS>(cG, scratch, totG);
+  const uint32_t eBefore = block_scan_excl<THREADS>(cE, scratch, totE);
+  const uint32_t skip = a.tie_break ? totE - need : 0u;  // LargestIndex takes the last `need` ties
+
+  // forced blocks that the score order did not pick are added on top (select_blocks)
+  uint32_t add_first = 0, add_last = 0;
+  if (forced) {
+    const uint32_t k0 = key_at(0), kl = key_at(n - 1);
+    const bool sel0 = k0 > T || (k0 == T && skip == 0);
+    const bool sell = kl > T || (kl == T && (totE - 1 >= skip) && (totE - 1 < skip + need));
+    add_first = sel0 ? 0u : 1u;
+    add_last = sell ? 0u : 1u;
+  }
+  const uint32_t tiesBefore = eBefore > skip ? min(eBefore - skip, need) : 0u;
+  uint32_t o = gBefore + tiesBefore + add_first;
+  uint32_t e = eBefore;
+  for (uint32_t i = s0; i < s1; ++i) {
+    const uint32_t key = key_at(i);
+    bool emit = key > T;
+    if (key == T) {
+      emit = (e >= skip) && (e < skip + need);
+      ++e;
+    }
+    if (emit) orow[o++] = position_of(i);
+  }
+  const uint32_t count = totG + need + add_first + add_last;
+  if (add_first && tid == 0) orow[0] = position_of(0);
+  if (add_last && tid == 0) orow[count - 1] = position_of(n - 1);
+  for (uint32_t i = count + tid; i < a.out_width; i += THREADS) orow[i] = -1;
+  if (a.out_count && tid == 0) a.out_count[row] = count;
+}
+
+// ---------------------------------------------------------------------------------------------------
+// dense work list (stage 1 and the flat indexer): chunk-major items, only tiles a chunk can need.
+// ---------------------------------------------------------------------------------------------------
+constexpr int kDenseThreads = 1024;
+constexpr int kDenseMaxChunks = 4096;
+
+__global__ void __launch_bounds__(kDenseThreads)
+build_dense_work_kernel(const uint32_t* __restrict__ pos, uint32_t nq, uint32_t chunk, uint32_t seq_len,
+                        uint32_t unit_div, uint32_t ntiles, WorkItem* __restrict__ work,
+                        uint32_t* __restrict__ work_count, uint32_t* __restrict__ work_cursor) {
+  __shared__ uint32_t offs[kDenseMaxChunks + 1];
+  __shared__ uint32_t scratch[64];
+  const uint32_t nchunks = (nq + chunk - 1) / chunk;
+  const uint32_t tid = threadIdx.x;
+  // tiles needed by each chunk
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < nchunks; base += kDenseThreads) {
+    const uint32_t c = base + tid;
+    uint32_t need = 0;
+    if (c < nchunks) {
+      uint32_t mp = 0;
+      const uint32_t q1 = min(nq, (c + 1) * chunk);
+      for (uint32_t q = c * chunk; q < q1; ++q) mp = max(mp, pos[q]);
+      mp = min(mp, seq_len - 1);
+      need = min(ntiles, (mp / unit_div) / kTileRows + 1);
+    }
+    uint32_t total;
+    const uint32_t before = block_scan_excl<kDenseThreads>(need, scratch, total);
+    if (c < nchunks) offs[c] = carry + before;
+    carry += total;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    offs[nchunks] = carry;
+    *work_count = carry;
+    *work_cursor = 0;
+  }
+  __syncthreads();
+  const uint32_t total_items = offs[nchunks];
+  for (uint32_t it = tid; it < total_items; it += kDenseThreads) {
+    uint32_t lo_c = 0, hi_c = nchunks;  // largest c with offs[c] <= it
+    while (hi_c - lo_c > 1) {
+      const uint32_t mid = (lo_c + hi_c) >> 1;
+      if (offs[mid] <= it) lo_c = mid; else hi_c = mid;
+    }
+    WorkItem w;
+    w.tile = it - offs[lo_c];
+    w.first = lo_c * chunk;
+    w.count = min(nq, (lo_c + 1) * chunk) - lo_c * chunk;
+    w.reserved = 0;
+    work[it] = w;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------------
+// list work (stage 2): per chunk of queries, group the (query, slot) pairs by selected block.
+// One CTA per chunk. pairs for chunk c live at [c*chunk*sel_stride, ...).
+// ---------------------------------------------------------------------------------------------------
+constexpr int kInvThreads = 256;
+
+__global__ void __launch_bounds__(kInvThreads)
+invert_selection_kernel(const int32_t* __restrict__ sel, const uint32_t* __restrict__ nsel, uint32_t sel_stride,
+                        uint32_t nq, uint32_t chunk, uint32_t num_blocks, uint32_t block_size,
+                        uint32_t segs_per_block, WorkItem* __restrict__ work, uint32_t* __restrict__ work_count,
+                        uint2* __restrict__ pairs) {
+  extern __shared__ __align__(16) uint32_t smem_u[];
+  uint32_t* cnt = smem_u;                  // [num_blocks]
+  uint32_t* off = smem_u + num_blocks;     // [num_blocks]
+  uint32_t* scratch = off + num_blocks;    // [64]
+  const uint32_t c = blockIdx.x, tid = threadIdx.x;
+  const uint32_t q0 = c * chunk, q1 = min(nq, q0 + chunk);
+  for (uint32_t b = tid; b < num_blocks; b += kInvThreads) cnt[b] = 0;
+  __syncthreads();
+  for (uint32_t q = q0 + tid; q < q1; q += kInvThreads) {
+    const uint32_t ns = nsel[q];
+    for (uint32_t s = 0; s < ns; ++s) atomicAdd(&cnt[uint32_t(sel[uint64_t(q) * sel_stride + s])], 1u);
+  }
+  __syncthreads();
+  // exclusive scan of counts and of the non-empty indicator, blocked over threads
+  const uint32_t per = (num_blocks + kInvThreads - 1) / kInvThreads;
+  const uint32_t b0 = min(num_blocks, tid * per), b1 = min(num_blocks, b0 + per);
+  uint32_t lsum = 0, lne = 0;
+  for (uint32_t b = b0; b < b1; ++b) { lsum += cnt[b]; lne += cnt[b] != 0; }
+  uint32_t tot_pairs, tot_ne;
+  uint32_t pre = block_scan_excl<kInvThreads>(lsum, scratch, tot_pairs);
+  uint32_t pne = block_scan_excl<kInvThreads>(lne, scratch, tot_ne);
+  if (tid == 0) scratch[48] = atomicAdd(work_count, tot_ne * segs_per_block);
+  __syncthreads();
+  const uint32_t item_base = scratch[48];
+  const uint32_t pair_base = q0 * sel_stride;
+  for (uint32_t b = b0; b < b1; ++b) {
+    const uint32_t n = cnt[b];
+    off[b] = pre;
+    if (n) {
+      for (uint32_t j = 0; j < segs_per_block; ++j) {
+        WorkItem w;
+        w.tile = b * segs_per_block + j;
+        w.first = pair_base + pre;
+        w.count = n;
+        w.reserved = 0;
+        work[item_base + pne * segs_per_block + j] = w;
+      }
+      ++pne;
+    }
+    pre += n;
+  }
+  __syncthreads();
+  for (uint32_t q = q0 + tid; q < q1; q += kInvThreads) {
+    const uint32_t ns = nsel[q];
+    for (uint32_t s = 0; s < ns; ++s) {
+      const uint32_t b = uint32_t(sel[uint64_t(q) * sel_stride + s]);
+      const uint32_t idx = atomicAdd(&off[b], 1u);
+      pairs[pair_base + idx] = make_uint2(q, s * block_size);
+    }
+  }
+}
+
+__global__ void zero_two_kernel(uint32_t* a, uint32_t* b) {
+  *a = 0;
+  *b = 0;
+}
+
+template <int THREADS, bool SMEM_KEYS>
+void launch_select_variant(const SelectArgs& args, uint32_t rows, uint32_t n_cap, cudaStream_t stream) {
+  const size_t smem = (size_t(kBins) + 64 + (SMEM_KEYS ? n_cap : 0)) * sizeof(uint32_t);
+  auto kern = select_rows_kernel<THREADS, SMEM_KEYS>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  kern<<<rows, THREADS, smem, stream>>>(args);
+}
+
+}  // namespace
+
+int launch_select(const SelectArgs& args, uint32_t rows, uint32_t n_cap, cudaStream_t stream) {
+  if (rows == 0) return 0;
+  if (n_cap <= 2048) launch_select_variant<128, true>(args, rows, n_cap, stream);
+  else if (n_cap <= 16384) launch_select_variant<256, true>(args, rows, n_cap, stream);
+  else if (n_cap <= 49152) launch_select_variant<1024, true>(args, rows, n_cap, stream);
+  else launch_select_variant<1024, false>(args, rows, n_cap, stream);
+  return 1;
+}
+
+int launch_build_dense_work(const uint32_t* pos, uint32_t nq, uint32_t chunk, uint32_t seq_len, uint32_t unit_div,
+                            uint32_t ntiles, WorkItem* work, uint32_t* work_count, uint32_t* work_cursor,
+                            cudaStream_t stream) {
+  if (nq == 0) return 0;
+  build_dense_work_kernel<<<1, kDenseThreads, 0, stream>>>(pos, nq, chunk, seq_len, unit_div, ntiles, work, work_count,
+                                                           work_cursor);
+  return 1;
+}
+
+int launch_invert_selection(const int32_t* sel, const uint32_t* nsel, uint32_t sel_stride, uint32_t nq, uint32_t chunk,
+                            uint32_t num_blocks, uint32_t block_size, uint32_t segs_per_block, WorkItem* work,
+                            uint32_t* work_count, uint32_t* work_cursor, uint2* pairs, cudaStream_t stream) {
+  if (nq == 0) return 0;
+  zero_two_kernel<<<1, 1, 0, stream>>>(work_count, work_cursor);
+  const size_t smem = (size_t(num_blocks) * 2 + 64) * sizeof(uint32_t);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(invert_selection_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  const uint32_t nchunks = (nq + chunk - 1) / chunk;
+  invert_selection_kernel<<<nchunks, kInvThreads, smem, stream>>>(sel, nsel, sel_stride, nq, chunk, num_blocks,
+                                                                  block_size, segs_per_block, work, work_count, pairs);
+  return 2;
+}
+
+int launch_expand_blocks(const int32_t* sel, const uint32_t* nsel, uint32_t sel_stride, const uint32_t* pos,
+                         uint32_t nq, uint32_t seq_len, uint32_t block_size, int32_t* out_idx, uint64_t out_stride,
+                         uint32_t out_width, uint32_t* out_count, cudaStream_t stream) {
+  // block_sparse_select (hisa/block_sparse.hpp:12-19) = the dense-regime path of the candidate select:
+  // keep >= every possible candidate count, so all causally valid tokens of the selected blocks are emitted.
+  SelectArgs a{};
+  a.scores = nullptr;
+  a.stride = 0;
+  a.pos = pos;
+  a.seq_len = seq_len;
+  a.block_size = block_size;
+  a.keep = 0xFFFFFFFFu;
+  a.mode = kSelCand;
+  a.sel = sel;
+  a.nsel = nsel;
+  a.sel_stride = sel_stride;
+  a.out_idx = out_idx;
+  a.out_stride = out_stride;
+  a.out_width = out_width;
+  a.out_count = out_count;
+  return launch_select(a, nq, 1, stream);
+}
+
+}  // namespace hisa_dev

@@ -1,0 +1,379 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle on identical seeded inputs.
+Bit-exact for integer/index work (lattice inputs, selection on given scores, block summaries); for fp scores
+the north-star rule: indices bit-exact except at near-ties (k-th/(k+1)-th gap below 1e-3 relative in bf16,
+1e-5 in fp32) and index-set recall >= 99.9 %."""
+import numpy as np
+import pytest
+
+from paper_2603_28458_b200 import capi
+from tests.gpu_helpers import compare_selection, indexer_for, round_problem_to_bf16
+
+pytestmark = pytest.mark.gpu
+
+BF16_RTOL = 1e-3
+F32_RTOL = 1e-5
+
+
+# ------------------------------------------------------------------------------------------ block summaries
+@pytest.mark.parametrize("L,B,d,dtype", [(1000, 128, 128, capi.DTYPE_BF16), (1000, 128, 8, capi.DTYPE_F32),
+                                         (4096, 64, 128, capi.DTYPE_BF16), (129, 128, 128, capi.DTYPE_F32),
+                                         (5, 4, 2, capi.DTYPE_F32)])
+def test_pool_build_matches_oracle_bit_exact(oracle, L, B, d, dtype):
+    rng = np.random.default_rng(L + B)
+    keys = rng.standard_normal((L, d)).astype(np.float32)
+    if dtype == capi.DTYPE_BF16:
+        keys = capi.bf16_bits_to_f32(capi.f32_to_bf16_bits(keys)).reshape(L, d)
+    cfg = capi.make_config(B, 64, 64, 4, d, dtype)
+    with capi.Indexer(cfg) as ix:
+        ix.upload_keys(keys)
+        ix.pool_build()
+        sums, counts, pooled = ix.pool_read()
+    osums, ocounts, opooled = oracle.pool_build(keys, B)
+    assert counts.tolist() == ocounts.tolist()
+    assert np.array_equal(sums, osums)       # same double additions in the same order
+    assert np.array_equal(pooled, opooled)
+
+
+def test_pool_append_equals_batch_and_oracle(oracle):
+    rng = np.random.default_rng(7)
+    L, B, d = 1500, 128, 128
+    keys = capi.bf16_bits_to_f32(capi.f32_to_bf16_bits(rng.standard_normal((L, d)).astype(np.float32))).reshape(L, d)
+    cfg = capi.make_config(B, 8, 8, 4, d, capi.DTYPE_BF16)
+    with capi.Indexer(cfg) as ix:
+        ix.upload_keys(keys[:300])
+        ix.pool_build()
+        at = 300
+        for n in (1, 1, B + 1, 27, 500, 128, 1):   # single tokens, block rollover, multi-block, exact fill
+            ix.pool_append(keys[at:at + n])
+            at += n
+        ix.pool_append(keys[at:])
+        assert ix.seq_len() == (L, (L + B - 1) // B)
+        sums, counts, pooled = ix.pool_read()
+    osums, ocounts, opooled = oracle.pool_build(keys, B, incremental=True)
+    assert counts.tolist() == ocounts.tolist()
+    assert np.array_equal(sums, osums) and np.array_equal(pooled, opooled)
+
+
+def test_pool_max_mode(oracle):
+    rng = np.random.default_rng(8)
+    keys = rng.standard_normal((300, 16)).astype(np.float32)
+    cfg = capi.make_config(32, 4, 4, 2, 16, capi.DTYPE_F32, pool_mode=1)
+    with capi.Indexer(cfg) as ix:
+        ix.upload_keys(keys[:100])
+        ix.pool_append(keys[100:])
+        _, counts, pooled = ix.pool_read()
+    _, ocounts, opooled = oracle.pool_build(keys, 32, mode=1)
+    assert counts.tolist() == ocounts.tolist() and np.array_equal(pooled, opooled)
+
+
+# ------------------------------------------------------------------------------------------ selection kernels
+@pytest.mark.parametrize("tb", [0, 1])
+@pytest.mark.parametrize("n_max,k", [(5, 2), (700, 50), (3000, 256), (9000, 2048), (20000, 2048), (70000, 2048)])
+def test_top_k_on_given_scores_bit_exact(oracle, tb, n_max, k):
+    rng = np.random.default_rng(n_max * 3 + tb)
+    rows = 24
+    n = rng.integers(1, n_max + 1, rows).astype(np.uint32)
+    n[0], n[1] = n_max, min(k, n_max)
+    scores = np.zeros((rows, n_max), np.float32)
+    for r in range(rows):
+        kind = r % 4
+        if kind == 0:
+            scores[r] = rng.standard_normal(n_max) * 40 + 300          # realistic: same sign/exponent
+        elif kind == 1:
+            scores[r] = rng.integers(-3, 4, n_max)                      # tie-saturated
+        elif kind == 2:
+            scores[r] = 7.0                                             # all equal
+        else:
+            scores[r] = rng.standard_normal(n_max) * np.float32(10.0) ** rng.integers(-30, 30, n_max)
+            scores[r, ::17] = 0.0
+            scores[r, 5::17] = -0.0                                     # signed zeros must tie
+    cfg = capi.make_config(128, 64, 2048, 4, 8, capi.DTYPE_F32, tie_break=tb)
+    with capi.Indexer(cfg) as ix:
+        idx, cnt = ix.top_k(scores, n, k)
+    for r in range(rows):
+        want = oracle.top_k(scores[r, :n[r]].astype(np.float64), np.arange(n[r]), k, tb)
+        assert cnt[r] == len(want)
+        assert idx[r, :cnt[r]].tolist() == want.tolist(), f"row {r} n={n[r]}"
+        assert (idx[r, cnt[r]:] == -1).all()
+
+
+@pytest.mark.parametrize("tb", [0, 1])
+@pytest.mark.parametrize("ffl,fib", [(True, False), (False, False), (True, True)])
+def test_select_blocks_on_given_scores_bit_exact(oracle, tb, ffl, fib):
+    rng = np.random.default_rng(11 + tb)
+    rows, M, m, B = 64, 600, 16, 8
+    ne = rng.integers(1, M + 1, rows).astype(np.uint32)
+    ne[:4] = [1, 2, m, m + 1]
+    J = np.where(rng.random((rows, M)) < 0.5, rng.integers(0, 6, (rows, M)), rng.standard_normal((rows, M)) * 5).astype(np.float32)
+    cfg = capi.make_config(B, m, m * B, 4, 8, capi.DTYPE_F32, force_first_last=ffl, forced_in_budget=fib, tie_break=tb)
+    with capi.Indexer(cfg) as ix:
+        blocks, nb = ix.select_blocks(J, ne)
+    p = oracle.Problem(np.zeros((1, 1, 1)), np.zeros((1, 1)), np.zeros((1, 1)), np.zeros(1, np.uint32), block_size=B,
+                       block_budget=m, token_budget=m * B, force_first_last=ffl, forced_in_budget=fib, tie_break=tb)
+    for r in range(rows):
+        t = (int(ne[r]) - 1) * B + 3
+        want = oracle.select_blocks(J[r, :ne[r]].astype(np.float64), np.arange(ne[r]), p, t)
+        assert blocks[r, :nb[r]].tolist() == want.tolist(), f"row {r} E={ne[r]}"
+        assert (blocks[r, nb[r]:] == -1).all()
+
+
+# ------------------------------------------------------------------------------------------ scorers
+@pytest.mark.parametrize("scorer", [capi.SCORER_SIMT, capi.SCORER_TENSOR])
+@pytest.mark.parametrize("dtype", [capi.DTYPE_BF16, capi.DTYPE_F32])
+def test_score_tokens_and_blocks_match_oracle(oracle, scorer, dtype):
+    L, Q, H, d, B = 700, 96, 64, 128, 128
+    pos = oracle.make_positions(L, Q, "spread")
+    prob = oracle.make_inputs("random", 5, L, pos, H, d, block_size=B, block_budget=8, token_budget=64)
+    if dtype == capi.DTYPE_BF16:
+        q, k = round_problem_to_bf16(prob)
+    else:
+        q, k = prob.queries, prob.keys
+    rtol = BF16_RTOL if dtype == capi.DTYPE_BF16 else F32_RTOL
+    with indexer_for(prob, dtype, scorer) as ix:
+        ix.upload_keys(k)
+        S = ix.score_tokens(q, prob.gates, pos)
+        J, ne = ix.score_blocks(q, prob.gates, pos)
+    for r in range(0, Q, 5):
+        t = int(pos[r])
+        want, _ = oracle.score_tokens(prob, r, np.arange(t + 1))
+        scale = np.abs(want).max()
+        assert np.abs(S[r, :t + 1] - want).max() <= rtol * scale * 0.05, f"row {r}"
+        wj = oracle.score_blocks(prob, r)
+        assert ne[r] == len(wj)
+        assert np.abs(J[r, :ne[r]] - wj).max() <= rtol * np.abs(wj).max() * 0.05, f"row {r} (blocks)"
+
+
+# ------------------------------------------------------------------------------------------ full pipeline
+@pytest.mark.parametrize("scorer", [capi.SCORER_SIMT, capi.SCORER_TENSOR])
+@pytest.mark.parametrize("shape", [
+    dict(L=1024, H=8, d=16, B=32, m=4, k=64),      # padded heads/dim, block smaller than a tile
+    dict(L=1536, H=64, d=128, B=128, m=3, k=300),  # native shape
+    dict(L=2048, H=64, d=64, B=256, m=2, k=300),   # block spans two tiles
+    dict(L=777, H=3, d=5, B=50, m=3, k=120),       # ragged everything
+])
+@pytest.mark.parametrize("tb", [0, 1])
+def test_lattice_inputs_bit_exact(oracle, scorer, shape, tb):
+    """Small-integer tensors: every product and sum is exact in bf16/fp32, so indices must equal the oracle's
+    exactly, including the tie-break order (hisa/synth.hpp:28-32 fixture)."""
+    L = shape["L"]
+    pos = np.arange(L, dtype=np.uint32)
+    prob = oracle.make_inputs("lattice", 3 + tb, L, pos, shape["H"], shape["d"], block_size=shape["B"],
+                              block_budget=shape["m"], token_budget=shape["k"], tie_break=tb)
+    q, k = round_problem_to_bf16(prob)   # integers: rounding is the identity
+    rows = np.unique(np.concatenate([np.arange(0, L, 13), [0, 1, L - 1, shape["k"] - 1, shape["k"], shape["m"] * shape["B"]]]))
+    rows = rows[rows < L]
+    with indexer_for(prob, capi.DTYPE_BF16, scorer) as ix:
+        ix.upload_keys(k)
+        h = ix.hisa_select(q, prob.gates, pos)
+        f = ix.dsa_select(q, prob.gates, pos)
+        b = ix.block_sparse_select(q, prob.gates, pos)
+    compare_selection(oracle, prob, "hisa", h, rows, 0.0, require_exact=True)
+    compare_selection(oracle, prob, "dsa", f, rows, 0.0, require_exact=True)
+    compare_selection(oracle, prob, "block", b, rows, 0.0, require_exact=True)
+    want = oracle.select_batch("hisa", prob, rows)
+    for i, r in enumerate(rows):
+        assert h["blocks"][r, :h["nblocks"][r]].tolist() == want.blocks[i, :want.nblocks[i]].tolist()
+        assert h["cand"][r] == want.cand[i]
+
+
+@pytest.mark.parametrize("ffl,fib", [(False, False), (True, True)])
+def test_lattice_forced_block_policies(oracle, ffl, fib):
+    L = 1024
+    pos = np.arange(L, dtype=np.uint32)
+    prob = oracle.make_inputs("lattice", 9, L, pos, 4, 8, block_size=32, block_budget=4, token_budget=100,
+                              force_first_last=ffl, forced_in_budget=fib)
+    q, k = round_problem_to_bf16(prob)
+    with indexer_for(prob) as ix:
+        ix.upload_keys(k)
+        h = ix.hisa_select(q, prob.gates, pos)
+    compare_selection(oracle, prob, "hisa", h, np.arange(0, L, 7), 0.0, require_exact=True)
+
+
+@pytest.mark.parametrize("dtype,rtol", [(capi.DTYPE_BF16, BF16_RTOL), (capi.DTYPE_F32, F32_RTOL)])
+def test_random_inputs_all_rows_near_tie_rule(oracle, dtype, rtol):
+    L = Q = 2048
+    H, d, B, m, k = 64, 128, 128, 4, 256
+    pos = np.arange(Q, dtype=np.uint32)
+    prob = oracle.make_inputs("random", 1, L, pos, H, d, block_size=B, block_budget=m, token_budget=k)
+    if dtype == capi.DTYPE_BF16:
+        q, kk = round_problem_to_bf16(prob)
+    else:
+        q, kk = prob.queries, prob.keys
+    with indexer_for(prob, dtype) as ix:
+        ix.upload_keys(kk, check_finite=True)
+        h = ix.hisa_select(q, prob.gates, pos, check_finite=True)
+        f = ix.dsa_select(q, prob.gates, pos)
+    rows = np.arange(Q)
+    ex_h, near_h, rec_h = compare_selection(oracle, prob, "hisa", h, rows, rtol)
+    ex_f, near_f, rec_f = compare_selection(oracle, prob, "dsa", f, rows, rtol)
+    print(f"hisa exact={ex_h} near-tie={near_h} recall={rec_h:.6f}; dsa exact={ex_f} near-tie={near_f} recall={rec_f:.6f}")
+    assert rec_h >= 0.999 and rec_f >= 0.999
+    assert ex_h + near_h == Q and ex_f + near_f == Q
+
+
+def test_reference_config_c1_sampled_rows_and_gpu_properties(oracle):
+    """BASELINE config[0] shape (L=8K, H=64, d=128, B=128, m=32, k=2048) with bf16 storage: oracle on a
+    stratified row sample; audit properties (hisa/audit.hpp:37-49) on ALL rows, GPU against GPU."""
+    L = Q = 8192
+    H, d, B, m, k = 64, 128, 128, 32, 2048
+    pos = np.arange(Q, dtype=np.uint32)
+    prob = oracle.make_inputs("random", 1, L, pos, H, d, block_size=B, block_budget=m, token_budget=k)
+    q, kk = round_problem_to_bf16(prob)
+    with indexer_for(prob) as ix:
+        ix.upload_keys(kk)
+        h = ix.hisa_select(q, prob.gates, pos)
+        f = ix.dsa_select(q, prob.gates, pos)
+    edge = [0, 1, B - 1, B, k - 1, k, k + 1, m * B - 1, m * B, m * B + 1, (m + 2) * B - 1, (m + 2) * B, L - B, L - 1]
+    rows = np.unique(np.concatenate([edge, np.random.default_rng(0).integers(0, L, 100)]))
+    _, _, rec_h = compare_selection(oracle, prob, "hisa", h, rows, BF16_RTOL)
+    _, _, rec_f = compare_selection(oracle, prob, "dsa", f, rows, BF16_RTOL)
+    assert rec_h >= 0.999 and rec_f >= 0.999
+    # regime equivalence: t + 1 <= mB  =>  hisa == dsa exactly (same kernels score the same pairs)
+    lim = m * B
+    assert np.array_equal(h["idx"][:lim], f["idx"][:lim]) and np.array_equal(h["count"][:lim], f["count"][:lim])
+    # dense regime: t + 1 <= k => the whole prefix
+    for t in (0, 1, 100, k - 1):
+        assert h["idx"][t, :t + 1].tolist() == list(range(t + 1)) and h["count"][t] == t + 1
+    # subset chain, cardinality, ordering on every row
+    t_col = pos[:, None].astype(np.int64)
+    valid = h["idx"] >= 0
+    assert (h["count"] == np.minimum(k, h["cand"])).all() and (valid.sum(1) == h["count"]).all()
+    assert ((h["idx"] <= t_col) | ~valid).all()
+    assert (np.diff(np.where(valid, h["idx"], np.iinfo(np.int32).max).astype(np.int64), axis=1) >= 0).all()
+    blk_of = np.where(valid, h["idx"] // B, -1)
+    for r in range(0, Q, 257):
+        assert set(blk_of[r][valid[r]].tolist()) <= set(h["blocks"][r, :h["nblocks"][r]].tolist())
+    assert (h["nblocks"] <= m + 2).all() and (h["blocks"][:, 0] == 0).all()
+    assert (h["blocks"][np.arange(Q), h["nblocks"] - 1] == pos // B).all()
+
+
+def test_decode_placement_and_streaming_position(oracle):
+    """Q=64 queries at the final position (QueryPlacement::Final), plus a streaming query at t == L."""
+    L, H, d, B, m, k = 4096, 64, 128, 128, 4, 512
+    pos = np.full(64, L - 1, np.uint32)
+    pos[-1] = L
+    prob = oracle.make_inputs("random", 2, L, pos, H, d, block_size=B, block_budget=m, token_budget=k)
+    q, kk = round_problem_to_bf16(prob)
+    with indexer_for(prob) as ix:
+        ix.upload_keys(kk[:L - 300])
+        ix.pool_build()
+        ix.pool_append(kk[L - 300:])     # decode-style incremental tail update
+        h = ix.hisa_select(q, prob.gates, pos)
+        f = ix.dsa_select(q, prob.gates, pos)
+    _, _, rec = compare_selection(oracle, prob, "hisa", h, np.arange(64), BF16_RTOL)
+    _, _, rec_f = compare_selection(oracle, prob, "dsa", f, np.arange(64), BF16_RTOL)
+    assert rec >= 0.999 and rec_f >= 0.999
+
+
+def test_clustered_inputs_recall(oracle):
+    L, H, d, B, m, k = 4096, 64, 128, 128, 8, 512
+    prob = oracle.make_inputs("clustered", 4, L, np.zeros(32, np.uint32), H, d, block_size=B, block_budget=m, token_budget=k)
+    q, kk = round_problem_to_bf16(prob)
+    with indexer_for(prob) as ix:
+        ix.upload_keys(kk)
+        h = ix.hisa_select(q, prob.gates, prob.positions)
+    _, _, rec = compare_selection(oracle, prob, "hisa", h, np.arange(32), BF16_RTOL)
+    assert rec >= 0.999
+
+
+# ------------------------------------------------------------------------------------------ SPEC worked examples on the GPU
+def test_spec_examples_through_the_cuda_path(oracle):
+    # SPEC.md:118 ReLU zeroes the negative dot; SPEC.md:119 negative gate cancels
+    cfg = capi.make_config(4, 1, 4, 1, 2, capi.DTYPE_F32)
+    with capi.Indexer(cfg) as ix:
+        ix.upload_keys(np.float32([[2, 0], [-1, 3]]))
+        s = ix.score_tokens(np.float32([[[1, 0]]]), np.float32([[1]]), np.uint32([1]))
+        assert s[0, :2].tolist() == [2.0, 0.0]
+    cfg = capi.make_config(4, 1, 4, 2, 2, capi.DTYPE_F32)
+    with capi.Indexer(cfg) as ix:
+        ix.upload_keys(np.float32([[1, 1]]))
+        s = ix.score_tokens(np.float32([[[1, 0], [0, 1]]]), np.float32([[1, -1]]), np.uint32([0]))
+        assert s[0, 0] == 0.0
+    # SPEC.md:128-129 top-k examples
+    cfg = capi.make_config(4, 1, 2, 1, 2, capi.DTYPE_F32)
+    with capi.Indexer(cfg) as ix:
+        idx, cnt = ix.top_k(np.float32([[5, 1, 3], [1, 1, 1]]), np.uint32([3, 3]), 2)
+        assert idx.tolist() == [[0, 2], [0, 1]] and cnt.tolist() == [2, 2]
+    # SPEC.md:138-139 dsa_select: t=3,k=10 -> whole prefix; L=1,k=1 -> {0}
+    cfg = capi.make_config(4, 4, 10, 2, 4, capi.DTYPE_F32)
+    rng = np.random.default_rng(0)
+    with capi.Indexer(cfg) as ix:
+        ix.upload_keys(rng.standard_normal((8, 4)).astype(np.float32))
+        r = ix.dsa_select(rng.standard_normal((1, 2, 4)).astype(np.float32), np.float32([[1, 1]]), np.uint32([3]))
+        assert r["idx"][0, :4].tolist() == [0, 1, 2, 3] and r["count"][0] == 4 and r["cand"][0] == 4
+    cfg = capi.make_config(1, 1, 1, 1, 1, capi.DTYPE_F32)
+    with capi.Indexer(cfg) as ix:
+        ix.upload_keys(np.float32([[1]]))
+        r = ix.dsa_select(np.float32([[[1]]]), np.float32([[1]]), np.uint32([0]))
+        assert r["idx"].tolist() == [[0]]
+    # SPEC.md:178 mean of two vectors; SPEC.md:188-189 append counts
+    cfg = capi.make_config(2, 1, 2, 1, 2, capi.DTYPE_F32)
+    with capi.Indexer(cfg) as ix:
+        ix.upload_keys(np.float32([[1, 2], [3, 4]]))
+        _, counts, pooled = ix.pool_read()
+        assert pooled.tolist() == [[2.0, 3.0]] and counts.tolist() == [2]
+        ix.pool_append(np.float32([[5, 6]]))
+        _, counts, pooled = ix.pool_read()
+        assert counts.tolist() == [2, 1] and pooled[1].tolist() == [5.0, 6.0]
+    # SPEC.md:208 select_blocks: J=[5,1,3,2], m=2 -> {0,2} U forced {0,3}
+    cfg = capi.make_config(4, 2, 8, 1, 2, capi.DTYPE_F32)
+    with capi.Indexer(cfg) as ix:
+        blocks, nb = ix.select_blocks(np.float32([[5, 1, 3, 2]]), np.uint32([4]))
+        assert blocks[0, :nb[0]].tolist() == [0, 2, 3]
+    # SPEC.md:220 candidate_union {0,2,3}, B=128, t=500 -> 373 tokens (via block-sparse select on crafted scores)
+    # SPEC.md:198 score_blocks: q=[1,0], pooled {[4,0],[-2,0]} -> [4, 0]
+    cfg = capi.make_config(1, 2, 2, 1, 2, capi.DTYPE_F32)
+    with capi.Indexer(cfg) as ix:
+        ix.upload_keys(np.float32([[4, 0], [-2, 0]]))
+        J, ne = ix.score_blocks(np.float32([[[1, 0]]]), np.float32([[1]]), np.uint32([1]))
+        assert J[0, :2].tolist() == [4.0, 0.0] and ne[0] == 2
+
+
+def test_eligible_block_count(oracle):
+    # t inside block 2 of 5 -> exactly 3 blocks scored
+    B = 4
+    cfg = capi.make_config(B, 5, 8, 2, 3, capi.DTYPE_F32)
+    rng = np.random.default_rng(1)
+    with capi.Indexer(cfg) as ix:
+        ix.upload_keys(rng.standard_normal((5 * B, 3)).astype(np.float32))
+        _, ne = ix.score_blocks(rng.standard_normal((1, 2, 3)).astype(np.float32), np.float32([[1, 1]]), np.uint32([2 * B + 1]))
+        assert ne[0] == 3
+
+
+# ------------------------------------------------------------------------------------------ errors (hisa/errors.hpp)
+def test_error_behaviour():
+    with pytest.raises(capi.HisaError) as e:
+        capi.Indexer(capi.make_config(128, 4, 2048, 64, 128))        # 4*128 < 2048
+    assert e.value.name == "InfeasibleConfig" and "mB >= k" in str(e.value)
+    with pytest.raises(capi.HisaError) as e:
+        capi.Indexer(capi.make_config(128, 64, 2048, 65, 128))
+    assert e.value.name == "Unsupported"
+    cfg = capi.make_config(4, 2, 4, 2, 4, capi.DTYPE_F32)
+    with capi.Indexer(cfg) as ix:
+        q, w, pos = np.zeros((1, 2, 4), np.float32), np.ones((1, 2), np.float32), np.uint32([0])
+        with pytest.raises(capi.HisaError) as e:
+            ix.hisa_select(q, w, pos)
+        assert e.value.name == "EmptySequence"
+        with pytest.raises(capi.HisaError) as e:
+            ix.upload_keys(np.zeros((0, 4), np.float32))
+        assert e.value.name == "EmptySequence"
+        ix.upload_keys(np.ones((8, 4), np.float32))
+        with pytest.raises(capi.HisaError) as e:
+            ix.pool_append(np.ones((1, 3), np.float32))
+        assert e.value.name == "DimensionMismatch"
+        bad = np.ones((8, 4), np.float32)
+        bad[3, 1] = np.inf
+        with pytest.raises(capi.HisaError) as e:
+            ix.upload_keys(bad, check_finite=True)
+        assert e.value.name == "NonFiniteValue"
+        ix.upload_keys(np.ones((8, 4), np.float32))
+        qbad = q.copy()
+        qbad[0, 1, 2] = np.nan
+        with pytest.raises(capi.HisaError) as e:
+            ix.hisa_select(qbad, w, pos, check_finite=True)
+        assert e.value.name == "NonFiniteValue"
+        with pytest.raises(capi.HisaError) as e:
+            ix.hisa_select(q, w, np.uint32([9]), check_finite=True)   # position > L
+        assert e.value.name == "ShapeMismatch"
+        r = ix.hisa_select(q, w, np.uint32([8]))                      # position == L is a streaming query
+        assert r["count"][0] == 4
