@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""bench.py — HISA hierarchical indexer throughput on B200 (metric of BASELINE.json).
+
+    python bench.py --gpus N --steps K --warmup W            # this repo's CUDA path
+    python bench.py --impl reference --gpus N --steps K ...  # the reference's CPU path (the oracle port)
+
+A "step" is one pass of the hot path over one batch of synthetic input: hisa_select for ALL query rows of
+the headline workload (C3: L=Q=65536, H=64, d=128, B=128, m=64, k=2048, bf16 q/k), inputs resident in HBM.
+Prints ONE JSON line (rank 0). See DESIGN.md §7 for how each field is measured.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "indexer queries/sec (HISA hierarchical top-k, full causal prefill)"
+UNIT = "queries/s"
+TILE_ROWS = 512  # query tile for round-robin sharding across ranks
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--seq-len", type=int, default=65536)
+    ap.add_argument("--block-size", type=int, default=128)
+    ap.add_argument("--block-budget", type=int, default=64)
+    ap.add_argument("--token-budget", type=int, default=2048)
+    ap.add_argument("--flat-steps", type=int, default=2, help="timed steps of the flat DSA comparison (0 = skip)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-rows", type=int, default=768, help="rows of the workload the CPU baseline is timed on")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=1)
+    return ap.parse_args()
+
+
+def workload_name(a):
+    return (f"C3 prefill L=Q={a.seq_len} H=64 d=128 B={a.block_size} m={a.block_budget} k={a.token_budget} "
+            f"bf16 q/k, fp32 gates, hisa_select")
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        p = json.load(open(path))
+        return {"tflops": float(p.get("bf16_tflops_sustained", p.get("bf16_tflops", 1400.0))),
+                "hbm_gbs": float(p.get("hbm_gbs", 6650.0)), "source": "measured (MEASURED_PEAKS.json, sustained bf16)"}
+    return {"tflops": 1400.0, "hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ------------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clocks and throttle reasons through NVML while the timed region runs."""
+
+    def __init__(self, index):
+        self.index, self.samples, self.reasons, self._stop = index, [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self.nv
+        names = {"hw_slowdown": 0x8, "sw_power_cap": 0x4, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "hw_power_brake_slowdown": 0x80, "sync_boost": 0x10}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for n, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------- sharding
+def rank_rows(Q, world, rank, tile=TILE_ROWS):
+    """Round-robin query tiles: causal work grows with the row index, so contiguous chunks would be
+    unbalanced. Returns the sorted row indices owned by `rank`."""
+    tiles = np.arange((Q + tile - 1) // tile)
+    mine = tiles[tiles % world == rank]
+    rows = (mine[:, None] * tile + np.arange(tile)[None, :]).reshape(-1)
+    return rows[rows < Q]
+
+
+def gathered_row_order(Q, world, tile=TILE_ROWS):
+    """Row index of every entry of the all-gathered [world, Q/world, k] buffer (rank-major)."""
+    return np.concatenate([rank_rows(Q, world, r, tile) for r in range(world)])
+
+
+# ------------------------------------------------------------------------------------------- reference arm
+def run_reference(a, rank, world):
+    """The reference's own CPU implementation of the path. The reference tree ships headers only for this
+    path (no .cpp, link fails), so the arm times the oracle port on all host cores, on a bounded sample of
+    the same workload; value = rows processed / time."""
+    if rank != 0:
+        return
+    from oracle import pyoracle
+    L = a.seq_len
+    rows_per_step = max(8, a.cpu_rows // 4)
+    rng = np.random.default_rng(a.seed)
+    keys = bf16_round(rng.standard_normal((L, 128), dtype=np.float32))
+    threads = pyoracle.hardware_threads()
+    times = []
+    for it in range(a.warmup + a.steps):
+        rows = np.sort(rng.choice(L, rows_per_step, replace=False)).astype(np.uint32)
+        q = bf16_round(rng.standard_normal((rows_per_step, 64, 128), dtype=np.float32))
+        w = rng.uniform(0.5, 1.5, (rows_per_step, 64)).astype(np.float32)
+        prob = pyoracle.Problem(q, w, keys, rows, block_size=a.block_size, block_budget=a.block_budget,
+                                token_budget=a.token_budget)
+        t0 = time.perf_counter()
+        pyoracle.select_batch("hisa", prob, threads=threads)
+        dt = time.perf_counter() - t0
+        if it >= a.warmup:
+            times.append(dt)
+    total = sum(times)
+    value = rows_per_step * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64 accumulate over bf16-rounded f32", "data": "synthetic",
+        "config": {"workload": workload_name(a), "sample": f"{rows_per_step} uniformly sampled query rows per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{rows_per_step} uniformly sampled rows of the workload per step, "
+                                   f"{len(times)} steps, all host threads (pool build excluded)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def bf16_round(x):
+    from paper_2603_28458_b200 import capi
+    return capi.bf16_bits_to_f32(capi.f32_to_bf16_bits(x)).reshape(x.shape)
+
+
+# ------------------------------------------------------------------------------------------- B200 arm
+def run_b200(a, rank, world, local_rank):
+    import torch
+    from paper_2603_28458_b200 import capi
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device — the product path has no CPU fallback")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        dist.init_process_group("nccl", device_id=dev)
+
+    L = Q = a.seq_len
+    H, d, B, m, k = 64, 128, a.block_size, a.block_budget, a.token_budget
+    g = torch.Generator(device=dev)
+    g.manual_seed(a.seed)
+    # keys: generated on rank 0 and replicated (NCCL broadcast over NVLink); queries: each rank generates only
+    # the rows it owns (synthetic, so nothing has to be scattered)
+    keys = torch.randn((L, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    if dist:
+        dist.broadcast(keys, src=0)
+    rows = rank_rows(Q, world, rank)
+    nq = len(rows)
+    g.manual_seed(a.seed + 1000 + rank)
+    q = torch.randn((nq, H, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    w = torch.rand((nq, H), generator=g, device=dev, dtype=torch.float32) + 0.5
+    pos = torch.from_numpy(rows.astype(np.int64)).to(dev).to(torch.int32)  # bit pattern == uint32 (values < 2^31)
+    out_idx = torch.empty((nq, k), device=dev, dtype=torch.int32)
+    out_count = torch.empty((nq,), device=dev, dtype=torch.int32)
+    out_cand = torch.empty((nq,), device=dev, dtype=torch.int32)
+    gathered = torch.empty((world * nq, k), device=dev, dtype=torch.int32) if dist else None
+    torch.cuda.synchronize()
+
+    cfg = capi.make_config(B, m, k, H, d, capi.DTYPE_BF16)
+    ix = capi.Indexer(cfg, local_rank)
+    ix.upload_keys(keys.data_ptr(), seq_len=L)
+    ix.pool_build()
+    ix.synchronize()
+    stream = torch.cuda.ExternalStream(capi.lib().hisa_cuda_stream(ix._ctx), device=dev)
+
+    def step_hisa():
+        ix.hisa_select_raw(q.data_ptr(), w.data_ptr(), pos.data_ptr(), nq, out_idx.data_ptr(), out_count.data_ptr(),
+                           None, None, out_cand.data_ptr())
+        if dist:
+            with torch.cuda.stream(stream):
+                dist.all_gather_into_tensor(gathered, out_idx)
+
+    def step_flat():
+        ix.dsa_select_raw(q.data_ptr(), w.data_ptr(), pos.data_ptr(), nq, out_idx.data_ptr(), out_count.data_ptr(), None)
+
+    def timed(fn, steps, warmup, profile=False):
+        for _ in range(warmup):
+            fn()
+        ix.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if profile:
+            ix.set_profiling(True)
+            ix.stage_times()  # reset accumulators
+        l0 = ix.launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record()
+        for _ in range(steps):
+            fn()
+        with torch.cuda.stream(stream):
+            e1.record()
+        ix.synchronize()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        stages = ix.stage_times() if profile else None
+        if profile:
+            ix.set_profiling(False)
+        launches = ix.launch_count() - l0
+        if dist:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms, stages, launches
+
+    with ClockSampler(local_rank) as clocks:
+        ms_total, stages, launches = timed(step_hisa, a.steps, a.warmup, profile=True)
+    ms_step = ms_total / a.steps
+    value = Q * a.steps / (ms_total * 1e-3)
+
+    # ---- roofline of the dominant kernel (stage-2 fused scorer): algorithmic flops / live CUDA-event time
+    cand_sum = int(out_cand.to(torch.int64).sum().item())
+    if dist:
+        t = torch.tensor([cand_sum], device=dev, dtype=torch.int64)
+        dist.all_reduce(t)
+        cand_sum_all = int(t.item())
+    else:
+        cand_sum_all = cand_sum
+    peaks = load_peaks()
+    flops_s2 = 2.0 * d * H * cand_sum          # this rank, one launch
+    k_ms = stages["score_tokens_ms"] / max(stages["calls"], 1)
+    achieved = flops_s2 / (k_ms * 1e-3) / 1e12 if k_ms > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_score_tc_stage2.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": "score_tc_kernel<1,2,4> (stage-2 block-major refinement)",
+                "achieved": achieved, "peak": peaks["tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["tflops"], "traffic": traffic, "peak_source": peaks["source"],
+                "flops_per_launch": flops_s2, "kernel_ms": k_ms}
+    per_call = {kk: (vv / max(stages["calls"], 1) if kk.endswith("_ms") else vv) for kk, vv in stages.items()}
+
+    # ---- in-run comparison: the flat DSA indexer built from the same kernels
+    flat = None
+    if a.flat_steps > 0:
+        fms, fstages, _ = timed(step_flat, a.flat_steps, 1, profile=True)
+        flat_step = fms / a.flat_steps
+        prefix = int((pos.to(torch.int64) + 1).sum().item())
+        fk_ms = fstages["score_tokens_ms"] / max(fstages["calls"], 1)
+        flat = {"ms_per_step": flat_step, "queries_per_s": Q / (flat_step * 1e-3), "hisa_speedup": flat_step / ms_step,
+                "scorer_ms": fk_ms, "top_k_ms": fstages["top_k_ms"] / max(fstages["calls"], 1),
+                "scorer_tflops": 2.0 * d * H * prefix / (fk_ms * 1e-3) / 1e12 if fk_ms > 0 else None}
+
+    # ---- end to end through the C ABI with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if a.e2e_steps > 0:
+        hq = torch.empty((nq, H, d), dtype=torch.bfloat16, pin_memory=True)
+        hw = torch.empty((nq, H), dtype=torch.float32, pin_memory=True)
+        hpos = torch.empty((nq,), dtype=torch.int32, pin_memory=True)
+        hidx = torch.empty((nq, k), dtype=torch.int32, pin_memory=True)
+        hcnt = torch.empty((nq,), dtype=torch.int32, pin_memory=True)
+        hq.copy_(q), hw.copy_(w), hpos.copy_(pos)
+        torch.cuda.synchronize()
+
+        def step_e2e():
+            ix.hisa_select_raw(hq.data_ptr(), hw.data_ptr(), hpos.data_ptr(), nq, hidx.data_ptr(), hcnt.data_ptr())
+
+        step_e2e()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(a.e2e_steps):
+            step_e2e()
+        ix.synchronize()
+        dt = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        same = bool(torch.equal(hidx.to(dev), out_idx)) if a.flat_steps == 0 else None
+        e2e = {"value": Q * a.e2e_steps / dt, "unit": UNIT,
+               "h2d_bytes_per_step": int(hq.numel() * 2 + hw.numel() * 4 + hpos.numel() * 4) * world,
+               "d2h_bytes_per_step": int(hidx.numel() * 4 + hcnt.numel() * 4) * world,
+               "ms_per_step": 1e3 * dt / a.e2e_steps, "matches_device_path": same}
+
+    # ---- CPU baseline: the oracle port on the host cores, bounded sample of the same workload (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        from oracle import pyoracle
+        nrows = a.cpu_rows
+        sel = np.sort(np.random.default_rng(0).choice(nq, nrows, replace=False))
+        sel_t = torch.from_numpy(sel).to(dev)
+        pq = q[sel_t].to(torch.float32).cpu().numpy()
+        pw = w[sel_t].cpu().numpy()
+        pk = keys.to(torch.float32).cpu().numpy()
+        prob = pyoracle.Problem(pq, pw, pk, rows[sel].astype(np.uint32), block_size=B, block_budget=m, token_budget=k)
+        threads = pyoracle.hardware_threads()
+        t0 = time.perf_counter()
+        ref = pyoracle.select_batch("hisa", prob, threads=threads)
+        dt = time.perf_counter() - t0
+        # the same rows double as a parity spot-check of the timed configuration
+        step_hisa()
+        ix.synchronize()
+        got = out_idx[sel_t].cpu().numpy()
+        inter = sum(len(set(got[i][got[i] >= 0].tolist()) & set(ref.idx[i, :ref.count[i]].tolist())) for i in range(nrows))
+        recall = inter / max(int(ref.count.sum()), 1)
+        cpu = {"value": nrows / dt, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{nrows} uniformly sampled query rows of the timed workload, all host threads, "
+                         f"pool build excluded; recall of the GPU result on these rows = {recall:.5f}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": workload_name(a), "l2": "inputs larger than L2 (q is 1 GiB per step)",
+                       "sharding": f"query tiles of {TILE_ROWS} rows round-robin over ranks; keys NCCL-broadcast; "
+                                   "indices all-gathered inside the step" if world > 1 else "single GPU"},
+            "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
+            "roofline": roofline, "cpu_baseline": cpu, "flat_dsa": flat, "stages_ms_per_step": per_call,
+            "candidate_pairs_per_step": cand_sum_all,
+        }
+        print(json.dumps(line), flush=True)
+    ix.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    if world != a.gpus and world == 1 and a.gpus > 1:
+        raise SystemExit("bench.py: --gpus N>1 must be launched with torch.distributed.run (one rank per GPU)")
+    run_b200(a, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -182,11 +182,12 @@ typedef struct hisa_cuda_stage_times {
   float top_k_ms;        /* final top-k               */
   float total_ms;        /* first kernel to last kernel of the call */
   uint64_t launches;     /* kernels launched by the call */
-  uint64_t work_items_stage1, work_items_stage2; /* scorer work items (tile x query-list units) */
+  uint64_t work_items_stage1, work_items_stage2; /* scorer work-item capacity (tile x query-list units) */
+  uint64_t calls;        /* API calls accumulated in this record */
 } hisa_cuda_stage_times;
 /* enable != 0: record CUDA events around every stage of subsequent calls (adds a few us). */
 int hisa_cuda_set_profiling(hisa_cuda_ctx* ctx, int enable);
-/* times of the last select call; synchronizes the context's stream. */
+/* Sums over all calls since the previous read (then resets); synchronizes the context's stream. */
 int hisa_cuda_last_stage_times(hisa_cuda_ctx* ctx, hisa_cuda_stage_times* out);
 /* total kernels launched on this context since creation */
 int hisa_cuda_launch_count(const hisa_cuda_ctx* ctx, uint64_t* launches);

@@ -54,6 +54,7 @@ class StageTimes(C.Structure):
         ("prepare_ms", C.c_float), ("score_blocks_ms", C.c_float), ("select_blocks_ms", C.c_float),
         ("invert_ms", C.c_float), ("score_tokens_ms", C.c_float), ("top_k_ms", C.c_float), ("total_ms", C.c_float),
         ("launches", C.c_uint64), ("work_items_stage1", C.c_uint64), ("work_items_stage2", C.c_uint64),
+        ("calls", C.c_uint64),
     ]
 
     def as_dict(self):

@@ -29,7 +29,7 @@ struct DevBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
-enum Stage { kStPrepare = 0, kStScoreBlocks, kStSelectBlocks, kStInvert, kStScoreTokens, kStTopK, kNumStages };
+enum Stage { kStPrepare = 0, kStScoreBlocks, kStSelectBlocks, kStInvert, kStScoreTokens, kStTopK, kStTotal, kNumStages };
 
 struct StageSpan {
   int stage;
@@ -71,7 +71,9 @@ struct hisa_cuda_ctx {
   size_t events_used = 0;
   uint64_t launches = 0, call_launches = 0;
   uint64_t items1 = 0, items2 = 0;
-  cudaEvent_t call_beg = nullptr, call_end = nullptr;
+  StageSpan call_span{};
+  bool call_open = false;
+  uint64_t calls = 0;
 
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
 };
@@ -402,21 +404,24 @@ int copy_out(hisa_cuda_ctx* ctx, void* dst, const void* src_dev, size_t bytes, b
   return HISA_OK;
 }
 
+// Profiling spans accumulate over every call since the last hisa_cuda_last_stage_times() read.
 void begin_call(hisa_cuda_ctx* ctx) {
-  ctx->call_launches = 0;
-  ctx->items1 = ctx->items2 = 0;
-  ctx->spans.clear();
-  ctx->events_used = 0;
+  ctx->calls += 1;
+  ctx->call_open = false;
   if (ctx->profiling) {
-    if (!ctx->call_beg) {
-      cudaEventCreate(&ctx->call_beg);
-      cudaEventCreate(&ctx->call_end);
-    }
-    cudaEventRecord(ctx->call_beg, ctx->stream);
+    ctx->call_span.stage = kStTotal;
+    ctx->call_span.beg = next_event(ctx);
+    ctx->call_span.end = next_event(ctx);
+    cudaEventRecord(ctx->call_span.beg, ctx->stream);
+    ctx->call_open = true;
   }
 }
 void end_call(hisa_cuda_ctx* ctx) {
-  if (ctx->profiling) cudaEventRecord(ctx->call_end, ctx->stream);
+  if (ctx->call_open) {
+    cudaEventRecord(ctx->call_span.end, ctx->stream);
+    ctx->spans.push_back(ctx->call_span);
+    ctx->call_open = false;
+  }
 }
 
 enum Strategy { kDsa = 0, kHisa = 1, kBlockSparse = 2 };
@@ -750,8 +755,6 @@ int hisa_cuda_destroy(hisa_cuda_ctx* ctx) {
                     &ctx->generic_scores, &ctx->generic_n, &ctx->export_a, &ctx->export_b, &ctx->flag})
     release(*b);
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
-  if (ctx->call_beg) cudaEventDestroy(ctx->call_beg);
-  if (ctx->call_end) cudaEventDestroy(ctx->call_end);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return HISA_OK;
@@ -1103,18 +1106,22 @@ int hisa_cuda_last_stage_times(hisa_cuda_ctx* ctx, hisa_cuda_stage_times* out) {
   if (!ctx || !out) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "null argument");
   memset(out, 0, sizeof *out);
   CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  float* slot[kNumStages] = {&out->prepare_ms,  &out->score_blocks_ms, &out->select_blocks_ms,
-                             &out->invert_ms,   &out->score_tokens_ms, &out->top_k_ms};
+  float* slot[kNumStages] = {&out->prepare_ms,  &out->score_blocks_ms, &out->select_blocks_ms, &out->invert_ms,
+                             &out->score_tokens_ms, &out->top_k_ms,     &out->total_ms};
   for (const StageSpan& s : ctx->spans) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, s.beg, s.end) == cudaSuccess) *slot[s.stage] += ms;
   }
-  if (ctx->profiling && ctx->call_beg && cudaEventQuery(ctx->call_end) == cudaSuccess)
-    cudaEventElapsedTime(&out->total_ms, ctx->call_beg, ctx->call_end);
   cudaGetLastError();
   out->launches = ctx->call_launches;
   out->work_items_stage1 = ctx->items1;
   out->work_items_stage2 = ctx->items2;
+  out->calls = ctx->calls;
+  ctx->spans.clear();
+  ctx->events_used = 0;
+  ctx->call_launches = 0;
+  ctx->items1 = ctx->items2 = 0;
+  ctx->calls = 0;
   return HISA_OK;
 }
 
