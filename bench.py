@@ -246,6 +246,7 @@ def run_b200(a, rank, world, local_rank):
         ms = e0.elapsed_time(e1)
         stages = ix.stage_times() if profile else None
         if profile:
+            stages["stalls"] = ix.scorer_stall_cycles()
             ix.set_profiling(False)
         launches = ix.launch_count() - l0
         if dist:
@@ -283,7 +284,12 @@ def run_b200(a, rank, world, local_rank):
                 "achieved": achieved, "peak": peaks["tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["tflops"], "traffic": traffic, "peak_source": peaks["source"],
                 "flops_per_launch": flops_s2, "kernel_ms": k_ms}
-    per_call = {kk: (vv / max(stages["calls"], 1) if kk.endswith("_ms") else vv) for kk, vv in stages.items()}
+    per_call = {kk: (vv / max(stages["calls"], 1) if kk.endswith("_ms") else vv) for kk, vv in stages.items()
+                if kk != "stalls"}
+    stalls = {}
+    for st_name, st in stages["stalls"].items():
+        cta = max(st["cta"], 1)
+        stalls[st_name] = {kk: (round(vv / cta, 4) if kk != "groups" else vv) for kk, vv in st.items() if kk != "cta"}
 
     # ---- in-run comparison: the flat DSA indexer built from the same kernels
     flat = None
@@ -363,6 +369,7 @@ def run_b200(a, rank, world, local_rank):
                                    "indices all-gathered inside the step" if world > 1 else "single GPU"},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
             "roofline": roofline, "cpu_baseline": cpu, "flat_dsa": flat, "stages_ms_per_step": per_call,
+            "scorer_stall_fraction_of_cta_time": stalls,
             "candidate_pairs_per_step": cand_sum_all,
         }
         print(json.dumps(line), flush=True)

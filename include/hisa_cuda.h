@@ -189,6 +189,11 @@ typedef struct hisa_cuda_stage_times {
 int hisa_cuda_set_profiling(hisa_cuda_ctx* ctx, int enable);
 /* Sums over all calls since the previous read (then resets); synchronizes the context's stream. */
 int hisa_cuda_last_stage_times(hisa_cuda_ctx* ctx, hisa_cuda_stage_times* out);
+/* Role-level stall accounting of the tensor-core scorer, collected while profiling is enabled: 16 counters
+ * per stage (cycles summed over all CTAs since the previous read; then reset). Index meaning:
+ * 0 CTA lifetime, 1 producer<-scheduler, 2 producer<-tile buffer, 3 producer<-query stage, 4 MMA<-query data,
+ * 5 MMA<-tile data, 6 MMA<-epilogue, 7 epilogue<-gates, 8 epilogue<-MMA, 9 epilogue busy, 10 groups. */
+int hisa_cuda_scorer_stall_cycles(hisa_cuda_ctx* ctx, uint64_t* stage1, uint64_t* stage2);
 /* total kernels launched on this context since creation */
 int hisa_cuda_launch_count(const hisa_cuda_ctx* ctx, uint64_t* launches);
 

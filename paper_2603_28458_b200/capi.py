@@ -27,7 +27,7 @@ EXPORTED_SYMBOLS = [
     "hisa_cuda_pool_build", "hisa_cuda_pool_append", "hisa_cuda_pool_read", "hisa_cuda_seq_len",
     "hisa_cuda_hisa_select", "hisa_cuda_dsa_select", "hisa_cuda_block_sparse_select", "hisa_cuda_score_blocks",
     "hisa_cuda_select_blocks", "hisa_cuda_score_tokens", "hisa_cuda_top_k", "hisa_cuda_set_profiling",
-    "hisa_cuda_last_stage_times", "hisa_cuda_launch_count",
+    "hisa_cuda_last_stage_times", "hisa_cuda_launch_count", "hisa_cuda_scorer_stall_cycles",
 ]
 
 
@@ -182,6 +182,14 @@ class Indexer:
         st = StageTimes()
         _check(lib().hisa_cuda_last_stage_times(self._ctx, C.byref(st)), self._ctx)
         return st.as_dict()
+
+    STALL_NAMES = ["cta", "prod_wait_sched", "prod_wait_tilebuf", "prod_wait_qstage", "mma_wait_qdata", "mma_wait_tile",
+                   "mma_wait_epilogue", "epi_wait_gates", "epi_wait_mma", "epi_busy", "groups"]
+
+    def scorer_stall_cycles(self) -> dict:
+        a, b = (C.c_uint64 * 16)(), (C.c_uint64 * 16)()
+        _check(lib().hisa_cuda_scorer_stall_cycles(self._ctx, a, b), self._ctx)
+        return {"stage1": dict(zip(self.STALL_NAMES, list(a))), "stage2": dict(zip(self.STALL_NAMES, list(b)))}
 
     def launch_count(self) -> int:
         n = C.c_uint64(0)

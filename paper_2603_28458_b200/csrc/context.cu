@@ -58,7 +58,7 @@ struct hisa_cuda_ctx {
 
   // per-call workspace
   DevBuf q_raw, q_op, gates_raw, gates_pad, pos, J, sel, nsel, work, pairs, scalars, cand, flat, out_idx, out_count,
-      out_cand, generic_scores, generic_n, export_a, export_b, flag;
+      out_cand, generic_scores, generic_n, export_a, export_b, flag, stats;
 
   // tuning
   uint32_t chunk_dense = 256, chunk_list = 512;
@@ -79,6 +79,8 @@ struct hisa_cuda_ctx {
 };
 
 namespace {
+
+uint32_t env_u32(const char* name, uint32_t dflt);
 
 int fail(hisa_cuda_ctx* ctx, int code, const char* fmt, ...) {
   char buf[1024];
@@ -252,10 +254,9 @@ int prepare_inputs(hisa_cuda_ctx* ctx, const void* queries, const float* gates, 
   // gates
   const float* g_dev = gates;
   if (!is_device_ptr(gates)) {
-    DevBuf& dst = (H == kHeads) ? ctx->gates_pad : ctx->gates_raw;
-    HISA_TRY(ensure(ctx, dst, size_t(Q) * H * sizeof(float)));
-    HISA_TRY(copy_in(ctx, dst.p, gates, size_t(Q) * H * sizeof(float)));
-    g_dev = dst.as<float>();
+    HISA_TRY(ensure(ctx, ctx->gates_raw, size_t(Q) * H * sizeof(float)));
+    HISA_TRY(copy_in(ctx, ctx->gates_raw.p, gates, size_t(Q) * H * sizeof(float)));
+    g_dev = ctx->gates_raw.as<float>();
   }
   if (check_finite) {
     HISA_TRY(ensure(ctx, ctx->flag, 16));
@@ -281,13 +282,10 @@ int prepare_inputs(hisa_cuda_ctx* ctx, const void* queries, const float* gates, 
                                             ctx->stream));
     out->q_op = ctx->q_op.as<__nv_bfloat16>();
   }
-  if (H == kHeads) {
-    out->gates = g_dev;
-  } else {
-    HISA_TRY(ensure(ctx, ctx->gates_pad, size_t(Q) * kHeads * sizeof(float)));
-    count_launches(ctx, launch_pad_gates(g_dev, Q, H, ctx->gates_pad.as<float>(), ctx->stream));
-    out->gates = ctx->gates_pad.as<float>();
-  }
+  // gates are always re-laid out (padded to 64 heads, permuted to the epilogue's lane order): 256 B per query
+  HISA_TRY(ensure(ctx, ctx->gates_pad, size_t(Q) * kHeads * sizeof(float)));
+  count_launches(ctx, launch_permute_gates(g_dev, Q, H, ctx->gates_pad.as<float>(), ctx->stream));
+  out->gates = ctx->gates_pad.as<float>();
   out->pos = pos_dev;
   out->Q = Q;
   return check_launch(ctx, "input preparation");
@@ -297,6 +295,7 @@ int prepare_inputs(hisa_cuda_ctx* ctx, const void* queries, const float* gates, 
 // scorer dispatch
 // ------------------------------------------------------------------------------------------------
 struct ScoreJob {
+  int stats_slot;  // 0: stage 1, 1: stage 2 / flat
   const __nv_bfloat16* a_op;
   uint64_t a_rows;
   uint32_t nseg_a;
@@ -329,13 +328,24 @@ int run_scorer(hisa_cuda_ctx* ctx, const ScoreJob& j) {
   a.nseg_b = ctx->nseg_q;
   for (int i = 0; i < kMaxSeg; ++i) a.terms[i] = j.terms[i];
   a.a_rows = uint32_t(j.a_rows);
+  a.debug_flags = env_u32("HISA_TC_DEBUG", 0);
+  a.stats = nullptr;
+  if (ctx->profiling) {
+    if (!ctx->stats.p) {
+      HISA_TRY(ensure(ctx, ctx->stats, 2 * 16 * sizeof(unsigned long long)));
+      CU_TRY(ctx, cudaMemsetAsync(ctx->stats.p, 0, 2 * 16 * sizeof(unsigned long long), ctx->stream));
+    }
+    a.stats = ctx->stats.as<unsigned long long>() + 16 * j.stats_slot;
+  }
   if (ctx->cfg.scorer == HISA_SCORER_SIMT) {
     count_launches(ctx, launch_score_simt(a, j.a_op, j.q_op, j.max_items, ctx->stream));
   } else {
     CUtensorMap map_a, map_b;
     HISA_TRY(make_map(ctx, &map_a, j.a_op, j.a_rows, uint64_t(j.nseg_a) * kDim, kTileRows));
     HISA_TRY(make_map(ctx, &map_b, j.q_op, j.nq * kHeads, uint64_t(ctx->nseg_q) * kDim, kHeads));
-    count_launches(ctx, launch_score_tc(a, map_a, map_b, ctx->num_sms, ctx->stream));
+    const int n = launch_score_tc(a, map_a, map_b, ctx->num_sms, ctx->stream);
+    if (n < 0) return fail(ctx, HISA_ERR_UNSUPPORTED, "no tensor-core scorer variant for this operand segment structure");
+    count_launches(ctx, n);
   }
   return check_launch(ctx, "scorer");
 }
@@ -490,6 +500,7 @@ int select_impl(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
         count_launches(ctx, launch_build_dense_work(p.pos + q0, uint32_t(nq), ctx->chunk_dense, L, 1, ntiles,
                                                     ctx->work.as<WorkItem>(), sc, sc + 1, ctx->stream));
         ScoreJob j{};
+        j.stats_slot = 1;
         j.a_op = ctx->key_op.as<__nv_bfloat16>();
         j.a_rows = L;
         j.nseg_a = ctx->nseg_k;
@@ -554,6 +565,7 @@ int select_impl(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
         {
           StageTimer timer(ctx, kStScoreTokens);
           ScoreJob j{};
+          j.stats_slot = 1;
           j.a_op = ctx->key_op.as<__nv_bfloat16>();
           j.a_rows = L;
           j.nseg_a = ctx->nseg_k;
@@ -752,7 +764,7 @@ int hisa_cuda_destroy(hisa_cuda_ctx* ctx) {
   for (DevBuf* b : {&ctx->key_op, &ctx->key_raw, &ctx->sums, &ctx->counts, &ctx->pooled_op, &ctx->q_raw, &ctx->q_op,
                     &ctx->gates_raw, &ctx->gates_pad, &ctx->pos, &ctx->J, &ctx->sel, &ctx->nsel, &ctx->work, &ctx->pairs,
                     &ctx->scalars, &ctx->cand, &ctx->flat, &ctx->out_idx, &ctx->out_count, &ctx->out_cand,
-                    &ctx->generic_scores, &ctx->generic_n, &ctx->export_a, &ctx->export_b, &ctx->flag})
+                    &ctx->generic_scores, &ctx->generic_n, &ctx->export_a, &ctx->export_b, &ctx->flag, &ctx->stats})
     release(*b);
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->stream);
@@ -1122,6 +1134,21 @@ int hisa_cuda_last_stage_times(hisa_cuda_ctx* ctx, hisa_cuda_stage_times* out) {
   ctx->call_launches = 0;
   ctx->items1 = ctx->items2 = 0;
   ctx->calls = 0;
+  return HISA_OK;
+}
+
+int hisa_cuda_scorer_stall_cycles(hisa_cuda_ctx* ctx, uint64_t* stage1, uint64_t* stage2) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  unsigned long long host[32] = {0};
+  if (ctx->stats.p) {
+    CU_TRY(ctx, cudaMemcpy(host, ctx->stats.p, sizeof host, cudaMemcpyDeviceToHost));
+    CU_TRY(ctx, cudaMemset(ctx->stats.p, 0, sizeof host));
+  }
+  for (int i = 0; i < 16; ++i) {
+    if (stage1) stage1[i] = host[i];
+    if (stage2) stage2[i] = host[16 + i];
+  }
   return HISA_OK;
 }
 

@@ -4,7 +4,8 @@
 //   key operand   bf16 [L_cap,  nseg_k * 128]   row s = key s, split into nseg_k bf16 segments, d padded to 128
 //   pooled operand bf16 [M_cap, nseg_p * 128]   row b = pooled key of block b (hi | lo [| lo2] split of the f32 mean)
 //   query operand bf16 [Q * 64, nseg_q * 128]   row t*64+j = head j of query t (heads padded to 64 with zeros)
-//   gates         f32  [Q, 64]                  padded with zeros
+//   gates         f32  [Q, 64]                  padded with zeros and PERMUTED: head j is stored at gate_slot(j),
+//                                               so that the 16 gates an epilogue lane needs are contiguous
 // A "tile" is 128 consecutive operand rows (the tcgen05 M extent); a "group" is 4 queries x 64 heads
 // (the tcgen05 N extent, 256 columns of TMEM).
 #pragma once
@@ -21,6 +22,10 @@ constexpr int kHeads = 64;      // heads per query in the operand (padded)
 constexpr int kDim = 128;       // elements per operand segment (padded d)
 constexpr int kGroupQ = 4;      // queries per MMA group (UMMA N = 256)
 constexpr int kMaxSeg = 3;
+
+// position of head j inside a query's 64-float gate row: heads {8r + 2c, 8r + 2c + 1 : r = 0..7} are the columns
+// that tcgen05.ld.16x256b hands to the lanes with (lane % 4) == c, and are stored as 16 consecutive floats.
+__host__ __device__ constexpr uint32_t gate_slot(uint32_t j) { return ((j % 8) / 2) * 16 + (j / 8) * 2 + (j % 2); }
 
 // One unit of scorer work: one operand tile against `count` queries.
 //   dense mode: queries are rows first .. first+count-1, results go to out[row, tile*128 + lane]
@@ -46,6 +51,24 @@ struct ScoreArgs {
   uint32_t nseg_a, nseg_b;     // operand segments of the tile (A) and query (B) operands
   uint32_t terms[kMaxSeg];     // terms[ib] = bit mask of A segments multiplied with B segment ib
   uint32_t a_rows;             // rows that exist in the A operand (rows beyond read as zero)
+  uint32_t debug_flags;        // timing experiments only (HISA_TC_DEBUG): 1 skip epilogue math, 2 skip query TMA
+  unsigned long long* stats;   // optional [kScoreStats] role-level stall cycles, summed over CTAs (may be null)
+};
+
+// indices into ScoreArgs::stats (cycles, summed over all CTAs of a launch)
+enum ScoreStat : int {
+  kStatCta = 0,          // CTA lifetime
+  kStatProdUnit,         // producer waiting for the scheduler
+  kStatProdAEmpty,       // producer waiting for a free tile buffer
+  kStatProdBEmpty,       // producer waiting for a free query stage
+  kStatMmaBFull,         // MMA issuer waiting for query data (TMA latency / bandwidth)
+  kStatMmaAFull,         // MMA issuer waiting for tile data
+  kStatMmaTEmpty,        // MMA issuer waiting for the epilogue to drain an accumulator
+  kStatEpiWFull,         // epilogue (warp 0) waiting for gates/meta
+  kStatEpiTFull,         // epilogue (warp 0) waiting for the MMA
+  kStatEpiBusy,          // epilogue (warp 0) cycles between t_full and t_empty arrive
+  kStatGroups,           // groups processed
+  kScoreStats
 };
 
 // tile -> first operand row and number of meaningful rows
@@ -89,7 +112,6 @@ int launch_score_tc(const ScoreArgs& args, const CUtensorMap& map_a, const CUten
                     cudaStream_t stream);
 int launch_score_simt(const ScoreArgs& args, const __nv_bfloat16* a_op, const __nv_bfloat16* q_op,
                       uint32_t max_items, cudaStream_t stream);
-size_t score_tc_smem_bytes(uint32_t nseg_a);
 
 int launch_select(const SelectArgs& args, uint32_t rows, uint32_t n_cap, cudaStream_t stream);
 
@@ -112,7 +134,7 @@ int launch_expand_blocks(const int32_t* sel, const uint32_t* nsel, uint32_t sel_
 int launch_convert_rows(const void* src, uint32_t src_is_bf16, uint64_t rows, uint32_t src_heads_or_1,
                         uint32_t src_dim, uint32_t nseg, __nv_bfloat16* dst, uint32_t dst_heads_or_1,
                         cudaStream_t stream);
-int launch_pad_gates(const float* src, uint64_t rows, uint32_t heads, float* dst, cudaStream_t stream);
+int launch_permute_gates(const float* src, uint64_t rows, uint32_t heads, float* dst, cudaStream_t stream);
 int launch_check_finite(const void* src, uint32_t is_bf16, uint64_t n, uint32_t* flag, cudaStream_t stream);
 int launch_check_positions(const uint32_t* pos, uint64_t n, uint32_t seq_len, uint32_t* flag, cudaStream_t stream);
 // block summaries over tokens [first, first+n): double sums, counts, pooled operand (nseg_p segments)

@@ -64,13 +64,14 @@ __global__ void convert_rows_kernel(const void* __restrict__ src, uint32_t src_i
     if (s < int(nseg)) *reinterpret_cast<uint4*>(drow_ptr + s * kDim + cg * 8) = *reinterpret_cast<const uint4*>(seg[s]);
 }
 
-__global__ void pad_gates_kernel(const float* __restrict__ src, uint64_t rows, uint32_t heads,
-                                 float* __restrict__ dst) {
+// pads the gates of a row to 64 heads and stores head j at gate_slot(j) (see kernels.cuh)
+__global__ void permute_gates_kernel(const float* __restrict__ src, uint64_t rows, uint32_t heads,
+                                     float* __restrict__ dst) {
   const uint64_t gid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gid >= rows * kHeads) return;
   const uint32_t h = uint32_t(gid % kHeads);
   const uint64_t r = gid / kHeads;
-  dst[gid] = h < heads ? src[r * heads + h] : 0.f;
+  dst[r * kHeads + gate_slot(h)] = h < heads ? src[r * heads + h] : 0.f;
 }
 
 __global__ void check_finite_kernel(const void* __restrict__ src, uint32_t is_bf16, uint64_t n,
@@ -145,9 +146,9 @@ int launch_convert_rows(const void* src, uint32_t src_is_bf16, uint64_t outer, u
   return 1;
 }
 
-int launch_pad_gates(const float* src, uint64_t rows, uint32_t heads, float* dst, cudaStream_t stream) {
+int launch_permute_gates(const float* src, uint64_t rows, uint32_t heads, float* dst, cudaStream_t stream) {
   if (rows == 0) return 0;
-  pad_gates_kernel<<<blocks_for(rows * kHeads, 256), 256, 0, stream>>>(src, rows, heads, dst);
+  permute_gates_kernel<<<blocks_for(rows * kHeads, 256), 256, 0, stream>>>(src, rows, heads, dst);
   return 1;
 }
 

@@ -55,7 +55,7 @@ score_simt_kernel(ScoreArgs a, const __nv_bfloat16* __restrict__ a_op, const __n
               const float* qv = s_q + ib * kDim;
               for (uint32_t i = 0; i < kDim; ++i) acc = fmaf(__bfloat162float(arow[i]), qv[i], acc);
             }
-        score = fmaf(a.gates[uint64_t(qrow) * kHeads + j], fmaxf(acc, 0.f), score);
+        score = fmaf(a.gates[uint64_t(qrow) * kHeads + gate_slot(j)], fmaxf(acc, 0.f), score);
       }
       if (r < valid) a.out[uint64_t(qrow) * a.out_stride + col + r] = score;
     }
