@@ -25,7 +25,6 @@ if ROOT not in sys.path:
 
 METRIC = "indexer queries/sec (HISA hierarchical top-k, full causal prefill)"
 UNIT = "queries/s"
-TILE_ROWS = 512  # query tile for round-robin sharding across ranks
 
 
 def parse_args():
@@ -110,18 +109,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------- sharding
-def rank_rows(Q, world, rank, tile=TILE_ROWS):
-    """Round-robin query tiles: causal work grows with the row index, so contiguous chunks would be
-    unbalanced. Returns the sorted row indices owned by `rank`."""
-    tiles = np.arange((Q + tile - 1) // tile)
-    mine = tiles[tiles % world == rank]
-    rows = (mine[:, None] * tile + np.arange(tile)[None, :]).reshape(-1)
-    return rows[rows < Q]
-
-
-def gathered_row_order(Q, world, tile=TILE_ROWS):
-    """Row index of every entry of the all-gathered [world, Q/world, k] buffer (rank-major)."""
-    return np.concatenate([rank_rows(Q, world, r, tile) for r in range(world)])
+from paper_2603_28458_b200.sharding import TILE_ROWS, rank_rows  # noqa: E402  (query tiles dealt zig-zag over ranks)
 
 
 # ------------------------------------------------------------------------------------------- reference arm

@@ -1,0 +1,219 @@
+// Drop-in test program: the worked examples and properties SPEC.md gives for the indexer path
+// (SPEC.md:118-120,128-130,138-140,178-180,188-190,198-200,208-210,218-220,228-235,427,461), written against
+// the reference's own hisa:: API and run on the GPU through libhisa_dropin.so. Exit code 0 = all passed.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <filesystem>
+#include <numeric>
+#include <sstream>
+
+#include "hisa/block_sparse.hpp"
+#include "hisa/bench.hpp"
+#include "hisa/hisa.hpp"
+#include "hisa/synth.hpp"
+#include "hisa/tensor_io.hpp"
+
+using namespace hisa;
+
+static int g_fail = 0, g_run = 0;
+#define EXPECT(cond)                                                              \
+  do {                                                                            \
+    ++g_run;                                                                      \
+    if (!(cond)) { ++g_fail; std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond); } \
+  } while (0)
+template <class E, class F>
+bool throws(F&& f) {
+  try { f(); } catch (const E&) { return true; } catch (...) { return false; }
+  return false;
+}
+
+static IndexerInputs tiny(std::vector<float> q, std::vector<float> w, std::vector<float> k, std::vector<uint32_t> pos,
+                          uint32_t H, uint32_t d) {
+  return IndexerInputs(std::move(q), std::move(w), std::move(k), std::move(pos), H, d);
+}
+
+// naive oracle for the DERIVED examples: triple loop in double
+static double naive_score(const IndexerInputs& in, uint32_t row, uint32_t s) {
+  double acc = 0;
+  for (uint32_t j = 0; j < in.num_heads(); ++j) {
+    double dp = 0;
+    for (uint32_t i = 0; i < in.dim(); ++i) dp += double(in.query(row, j)[i]) * double(in.key(s)[i]);
+    acc += double(in.gate(row, j)) * std::max(dp, 0.0);
+  }
+  return acc;
+}
+static std::vector<uint32_t> naive_topk(const std::vector<double>& sc, const std::vector<uint32_t>& pos, uint32_t k, TieBreak tb) {
+  std::vector<uint32_t> order(sc.size());
+  std::iota(order.begin(), order.end(), 0u);
+  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    if (sc[a] != sc[b]) return sc[a] > sc[b];
+    return tb == TieBreak::SmallestIndex ? pos[a] < pos[b] : pos[a] > pos[b];
+  });
+  order.resize(std::min<size_t>(k, order.size()));
+  std::vector<uint32_t> out;
+  for (uint32_t i : order) out.push_back(pos[i]);
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+int main() {
+  // ---- config ----
+  EXPECT(throws<InfeasibleConfig>([] { HisaConfig c(128, 4, 2048, 64, 128); (void)c; }));
+  EXPECT(!throws<InfeasibleConfig>([] { HisaConfig c(128, 16, 2048, 4, 64); (void)c; }));
+  EXPECT(strategy_from_string("block-sparse") == Strategy::BlockSparse && to_string(Strategy::Hisa) == "hisa");
+
+  // ---- score_tokens ----
+  {
+    auto in = tiny({1, 0}, {1}, {2, 0, -1, 3}, {1}, 1, 2);
+    const uint32_t cand[] = {0, 1};
+    OpCounter c;
+    auto sv = score_tokens(in, 0, cand, &c);
+    EXPECT(sv.scores[0] == 2.0 && sv.scores[1] == 0.0 && c.dot_products == 2);
+    auto in2 = tiny({1, 0, 0, 1}, {1, -1}, {1, 1}, {0}, 2, 2);
+    const uint32_t c0[] = {0};
+    EXPECT(score_tokens(in2, 0, c0).scores[0] == 0.0);
+    auto in3 = tiny({1, 0}, {1}, {2, 0, -1, 3}, {0}, 1, 2);
+    EXPECT(throws<CausalViolation>([&] { score_tokens(in3, 0, cand); }));
+    Rng rng(5);
+    auto r = make_random_inputs(rng, 32, 3, 4, 16, QueryPlacement::Final);
+    std::vector<uint32_t> all(32);
+    std::iota(all.begin(), all.end(), 0u);
+    auto got = score_tokens(r, 1, all);
+    double worst = 0;
+    for (uint32_t s = 0; s < 32; ++s) worst = std::max(worst, std::abs(got.scores[s] - naive_score(r, 1, s)));
+    EXPECT(worst < 1e-5 * 50);  // SPEC tolerance 1e-5 on O(1) scores; these reach ~50
+  }
+  // ---- top_k_tokens ----
+  {
+    ScoreVector sv{{5, 1, 3}, {0, 1, 2}};
+    EXPECT((top_k_tokens(sv, 2, TieBreak::SmallestIndex).token_indices == std::vector<uint32_t>{0, 2}));
+    ScoreVector ties{{1, 1, 1}, {0, 1, 2}};
+    EXPECT((top_k_tokens(ties, 2, TieBreak::SmallestIndex).token_indices == std::vector<uint32_t>{0, 1}));
+    EXPECT((top_k_tokens(ties, 2, TieBreak::LargestIndex).token_indices == std::vector<uint32_t>{1, 2}));
+    EXPECT(top_k_tokens(ties, 9, TieBreak::SmallestIndex).token_indices.size() == 3);
+    Rng rng(9);
+    for (int trial = 0; trial < 20; ++trial) {
+      ScoreVector v;
+      const uint32_t n = 1 + uint32_t(rng.below(1000));
+      for (uint32_t i = 0; i < n; ++i) { v.scores.push_back(trial % 2 ? double(rng.below(7)) : double(float(rng.normal()))); v.positions.push_back(3 * i + 1); }
+      const TieBreak tb = trial % 3 ? TieBreak::SmallestIndex : TieBreak::LargestIndex;
+      EXPECT(top_k_tokens(v, 50, tb).token_indices == naive_topk(v.scores, v.positions, 50, tb));
+    }
+  }
+  // ---- block summaries ----
+  {
+    const std::vector<float> k2 = {1, 2, 3, 4};
+    auto c = build_block_summaries(k2, 2, 2);
+    EXPECT(c.num_blocks() == 1 && c.pooled(0)[0] == 2.0 && c.pooled(0)[1] == 3.0);
+    EXPECT(throws<EmptySequence>([] { build_block_summaries(std::span<const float>{}, 2, 2); }));
+    BlockSummaryCache inc(4, 3);
+    const std::vector<float> key = {1, 2, 3};
+    inc.append(key);
+    EXPECT(inc.count(0) == 1 && inc.pooled(0)[2] == 3.0);
+    for (int i = 0; i < 4; ++i) inc.append(key);
+    EXPECT(inc.num_blocks() == 2 && inc.count(0) == 4 && inc.count(1) == 1);
+    const std::vector<float> bad = {1, 2};
+    EXPECT(throws<DimensionMismatch>([&] { inc.append(bad); }));
+    EXPECT(throws<Error>([&] { inc.pooled(7); }));
+    Rng rng(3);
+    std::vector<float> keys(1000 * 8);
+    for (auto& v : keys) v = float(rng.normal());
+    auto batch = build_block_summaries(keys, 8, 128);
+    BlockSummaryCache stream(128, 8);
+    for (int s = 0; s < 1000; ++s) stream.append(std::span<const float>(&keys[s * 8], 8));
+    EXPECT(batch.num_blocks() == 8 && batch.count(7) == 104);
+    double worst = 0;
+    for (uint32_t b = 0; b < 8; ++b)
+      for (uint32_t i = 0; i < 8; ++i) worst = std::max(worst, std::abs(batch.pooled(b)[i] - stream.pooled(b)[i]));
+    EXPECT(worst <= 1e-6);  // SPEC.md:80 (device kernel and host append agree; in fact bit for bit)
+    EXPECT(worst == 0.0);
+  }
+  // ---- score_blocks / select_blocks / candidate_union ----
+  {
+    auto in = tiny({1, 0}, {1}, {4, 0, -2, 0}, {1}, 1, 2);
+    auto cache = build_block_summaries(in.keys_raw(), 2, 1);
+    auto J = score_blocks(in, cache, 0);
+    EXPECT(J.scores.size() == 2 && J.scores[0] == 4.0 && J.scores[1] == 0.0);
+    HisaConfig cfg(4, 2, 8, 1, 2);
+    ScoreVector js{{5, 1, 3, 2}, {0, 1, 2, 3}};
+    EXPECT((select_blocks(js, cfg, 15) == std::vector<uint32_t>{0, 2, 3}));
+    HisaConfig wide(4, 9, 8, 1, 2);
+    EXPECT((select_blocks(js, wide, 15) == std::vector<uint32_t>{0, 1, 2, 3}));
+    const uint32_t b0[] = {0}, b1[] = {1}, b023[] = {0, 2, 3};
+    EXPECT((candidate_union(b0, 4, 10, 100) == std::vector<uint32_t>{0, 1, 2, 3}));
+    EXPECT((candidate_union(b1, 4, 5, 100) == std::vector<uint32_t>{4, 5}));
+    EXPECT(candidate_union(b023, 128, 500, 4096).size() == 373);
+  }
+  // ---- dsa_select / hisa_select regimes ----
+  {
+    Rng rng(11);
+    const uint32_t L = 4096, H = 4, d = 16, B = 64, m = 8, k = 256;
+    std::vector<uint32_t> pos = {0, 3, k - 1, k, m * B - 1, m * B, (m + 2) * B + 5, 2000, L - 1};
+    auto in = make_random_inputs(rng, L, pos, H, d);
+    HisaConfig cfg(B, m, k, H, d);
+    auto cache = build_block_summaries(in.keys_raw(), d, B);
+    for (uint32_t r = 0; r < pos.size(); ++r) {
+      OpCounter ch, cd;
+      auto h = hisa_select(in, cache, cfg, r, &ch);
+      auto f = dsa_select(in, cfg, r, &cd);
+      const uint32_t t = pos[r];
+      EXPECT(std::is_sorted(h.token_indices.begin(), h.token_indices.end()));
+      EXPECT(f.token_indices.size() == std::min(k, t + 1) && f.candidate_size == t + 1 && f.selected_blocks.empty());
+      EXPECT(cd.dot_products == uint64_t(H) * (t + 1));
+      if (t + 1 <= k) {
+        std::vector<uint32_t> prefix(t + 1);
+        std::iota(prefix.begin(), prefix.end(), 0u);
+        EXPECT(h.token_indices == prefix);
+      }
+      if (t + 1 <= m * B) EXPECT(h.token_indices == f.token_indices);
+      auto omega = candidate_union(h.selected_blocks, B, t, L);
+      EXPECT(h.candidate_size == omega.size() && h.token_indices.size() == std::min<size_t>(k, omega.size()));
+      EXPECT(std::includes(omega.begin(), omega.end(), h.token_indices.begin(), h.token_indices.end()));
+      EXPECT(h.selected_blocks.size() <= m + 2 && h.selected_blocks.front() == 0 && h.selected_blocks.back() == t / B);
+      EXPECT(ch.dot_products <= analytic_cost(cfg, t + 1, Strategy::Hisa));
+      // T equals the brute-force flat selection restricted to the candidate pool
+      std::vector<double> sc;
+      for (uint32_t s : omega) sc.push_back(naive_score(in, r, s));
+      auto want = naive_topk(sc, omega, k, cfg.tie_break);
+      size_t same = 0;
+      for (uint32_t v : h.token_indices) same += std::binary_search(want.begin(), want.end(), v);
+      EXPECT(same + 1 >= want.size());  // identical up to one fp32-vs-f64 near-tie at the k-th score
+      auto bs = block_sparse_select(in, cache, cfg, r);
+      EXPECT(bs.token_indices == omega);
+    }
+  }
+  // ---- analytic cost and the bench record ----
+  {
+    HisaConfig cfg(128, 64, 2048, 1, 16);
+    EXPECT(analytic_cost(cfg, 65536, Strategy::Hisa) == 8960 && analytic_cost(cfg, 65536, Strategy::Dsa) == 65536);
+    HisaConfig small(32, 4, 64, 4, 16);
+    auto rec = run_bench(small, 1024, 16, 1, Strategy::Dsa);
+    EXPECT(rec.dot_products == uint64_t(16) * 4 * 1024 && rec.wall_ns_median > 0);
+    auto rh = run_bench(small, 1024, 16, 1, Strategy::Hisa);
+    EXPECT(rh.dot_products <= rh.analytic_bound);
+    std::ostringstream os;
+    write_bench_csv(os, {rec, rh});
+    EXPECT(os.str().rfind("strategy,L,B,m,k,H,d,wall_ns_median", 0) == 0);
+  }
+  // ---- HSB round trip ----
+  {
+    Rng rng(2);
+    auto in = make_random_inputs(rng, 20, 3, 2, 4, QueryPlacement::Spread);
+    const auto path = std::filesystem::temp_directory_path() / "hisa_dropin_test.hsb";
+    save_tensor_file(in, path);
+    auto back = load_tensor_file(path);
+    EXPECT(back.keys_raw() == in.keys_raw() && back.queries_raw() == in.queries_raw() && back.gates_raw() == in.gates_raw() &&
+           back.positions_raw() == in.positions_raw() && back.num_heads() == 2 && back.dim() == 4);
+    {
+      std::FILE* f = std::fopen(path.c_str(), "r+b");
+      std::fputc('X', f);
+      std::fclose(f);
+    }
+    EXPECT(throws<BadMagic>([&] { load_tensor_file(path); }));
+    std::filesystem::remove(path);
+    EXPECT(throws<IoError>([&] { load_tensor_file(path); }));
+  }
+  std::printf("%s: %d checks, %d failed\n", g_fail ? "FAILED" : "PASSED", g_run, g_fail);
+  return g_fail ? 1 : 0;
+}

@@ -1,0 +1,47 @@
+"""The C++ host layer (the reference's hisa:: entry points over the C ABI).
+CPU: the library builds, links only against the C ABI and exports the reference's symbols.
+GPU: paper_2603_28458_b200/cpp/test_dropin.cpp runs the SPEC examples through that API on the device."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIBDIR = os.path.join(ROOT, "paper_2603_28458_b200", "_lib")
+
+
+@pytest.fixture(scope="module")
+def built():
+    from paper_2603_28458_b200 import capi
+    capi.build()
+    subprocess.run(["make", "-C", os.path.join(ROOT, "paper_2603_28458_b200", "cpp"), "-j4"], check=True, capture_output=True)
+    return LIBDIR
+
+
+def test_dropin_exports_reference_entry_points(built):
+    out = subprocess.run(["nm", "-D", "--defined-only", "-C", os.path.join(built, "libhisa_dropin.so")],
+                         check=True, capture_output=True, text=True).stdout
+    for sym in ["hisa::score_tokens(", "hisa::top_k_tokens(", "hisa::dsa_select(", "hisa::score_blocks(",
+                "hisa::select_blocks(", "hisa::candidate_union(", "hisa::hisa_select(", "hisa::block_sparse_select(",
+                "hisa::build_block_summaries(", "hisa::BlockSummaryCache::append(", "hisa::BlockSummaryCache::pooled(",
+                "hisa::IndexerInputs::IndexerInputs(", "hisa::make_random_inputs(", "hisa::load_tensor_file(",
+                "hisa::save_tensor_file(", "hisa::parallel_for(", "hisa::worker_count(", "hisa::analytic_cost(",
+                "hisa::run_bench(", "hisa::write_bench_csv(", "hisa::to_string(", "hisa::strategy_from_string(",
+                "hisa::gpu::Indexer::hisa_select_batch("]:
+        assert sym in out, f"{sym} not exported by libhisa_dropin.so"
+
+
+def test_dropin_host_layer_has_no_cuda_dependency_of_its_own(built):
+    # the C++ layer reaches the device only through hisa_cuda_* (the thin C ABI)
+    und = subprocess.run(["nm", "-D", "--undefined-only", os.path.join(built, "libhisa_dropin.so")],
+                         check=True, capture_output=True, text=True).stdout
+    assert "hisa_cuda_hisa_select" in und and "hisa_cuda_create" in und
+    assert "cudaMalloc" not in und and "cuLaunch" not in und
+
+
+@pytest.mark.gpu
+def test_dropin_spec_examples_on_gpu(built):
+    r = subprocess.run([os.path.join(built, "test_dropin")], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-3000:], r.stderr[-2000:])
+    assert r.returncode == 0, r.stdout[-3000:]
+    assert "PASSED" in r.stdout
