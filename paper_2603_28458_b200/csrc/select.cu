@@ -22,6 +22,7 @@ namespace {
 
 constexpr int kBins = 2048;
 constexpr int kBinBits = 11;
+constexpr int kListCap = 1024;  // survivors of the first radix level are compacted when they fit here
 
 __device__ __forceinline__ uint32_t score_key(float f) {
   uint32_t b = __float_as_uint(f);
@@ -83,9 +84,11 @@ __device__ __forceinline__ uint32_t block_reduce_max(uint32_t v, uint32_t* scrat
 template <int THREADS, bool SMEM_KEYS>
 __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
   extern __shared__ __align__(16) uint32_t smem_u[];
-  uint32_t* hist = smem_u;               // [kBins]
-  uint32_t* scratch = smem_u + kBins;    // [64]
-  uint32_t* skey = smem_u + kBins + 64;  // [n_cap] when SMEM_KEYS
+  uint32_t* hist = smem_u;                // [kBins]
+  uint32_t* scratch = smem_u + kBins;     // [64]
+  uint32_t* list = smem_u + kBins + 64;   // [kListCap]
+  uint32_t* ssel = list + kListCap;       // [sel_stride] the row's selected blocks (candidate mode)
+  uint32_t* skey = ssel + a.sel_stride;   // [n_cap] when SMEM_KEYS (16-byte aligned: sel_stride is padded to 4)
 
   const uint32_t row = blockIdx.x;
   const uint32_t tid = threadIdx.x;
@@ -104,9 +107,11 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
   } else if (a.mode == kSelCand) {
     const uint32_t t = min(a.pos[row], a.seq_len - 1);
     const uint32_t ns = a.nsel[row];
-    sel_row = a.sel + uint64_t(row) * a.sel_stride;
+    sel_row = a.sel + uint64_t(row) * a.sel_row_stride;
     const uint32_t lastb = uint32_t(sel_row[ns - 1]);
     n = (ns - 1) * B + min(B, t - lastb * B + 1);
+    for (uint32_t i = tid; i < ns; i += THREADS) ssel[i] = uint32_t(sel_row[i]);
+    __syncthreads();
   } else {
     n = a.n_in[row];
   }
@@ -115,8 +120,12 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
   const uint32_t keep = a.keep;
   const bool forced = block_mode && a.force_first_last && n > 0;
 
+  const uint32_t bshift = a.block_shift;  // log2(B) when B is a power of two, else 32
   auto position_of = [&](uint32_t i) -> int32_t {
-    if (a.mode == kSelCand) return sel_row[i / B] * int32_t(B) + int32_t(i % B);
+    if (a.mode == kSelCand) {
+      const uint32_t slot = bshift < 32 ? i >> bshift : i / B;
+      return int32_t(ssel[slot] * B + (i - slot * B));
+    }
     return int32_t(i);
   };
 
@@ -141,27 +150,61 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
 
   // ---- keys, min, max ---------------------------------------------------------------------------
   uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
-  for (uint32_t i = tid; i < n; i += THREADS) {
-    const uint32_t key = raw_key(i);
-    if constexpr (SMEM_KEYS) skey[i] = key;
-    kmin = min(kmin, key);
-    kmax = max(kmax, key);
+  const bool boost = forced && a.forced_in_budget;
+  if (SMEM_KEYS && a.vec_ok && !boost) {
+    // 16-byte loads: four scores per request keep enough bytes in flight at 5 CTAs per SM
+    const float4* s4 = reinterpret_cast<const float4*>(srow);
+    const uint32_t n4 = n >> 2;
+    for (uint32_t i = tid; i < n4; i += THREADS) {
+      const float4 v = __ldg(s4 + i);
+      uint4 kq;
+      kq.x = score_key(v.x); kq.y = score_key(v.y); kq.z = score_key(v.z); kq.w = score_key(v.w);
+      reinterpret_cast<uint4*>(skey)[i] = kq;
+      kmin = min(min(kmin, kq.x), min(min(kq.y, kq.z), kq.w));
+      kmax = max(max(kmax, kq.x), max(max(kq.y, kq.z), kq.w));
+    }
+    for (uint32_t i = (n4 << 2) + tid; i < n; i += THREADS) {
+      const uint32_t key = score_key(srow[i]);
+      skey[i] = key;
+      kmin = min(kmin, key);
+      kmax = max(kmax, key);
+    }
+  } else {
+    for (uint32_t i = tid; i < n; i += THREADS) {
+      const uint32_t key = raw_key(i);
+      if constexpr (SMEM_KEYS) skey[i] = key;
+      kmin = min(kmin, key);
+      kmax = max(kmax, key);
+    }
   }
   uint32_t lo = block_reduce_min<THREADS>(kmin, scratch);
   uint32_t hi = block_reduce_max<THREADS>(kmax, scratch);
   __syncthreads();
 
   // ---- range-adaptive radix select of the keep-th largest key ------------------------------------
+  // (tried and measured on B200, both dropped: a compare-and-count bisection instead of the histogram was 45 %
+  //  slower — ~30 block-wide count steps per row cost more than three 11-bit levels, two of them on the survivor
+  //  list; a sample-guided bracket that restricts the first level to ~20 % of the keys changed nothing — the
+  //  kernel is spread over many short phases, not bound by the shared-memory atomics)
   uint32_t kk = keep;  // still to take from [lo, hi]
+  bool use_list = false;
+  uint32_t list_n = 0;
   while (lo != hi) {
     const uint32_t range = hi - lo;
     const uint32_t nb = 32 - __clz(range);
     const uint32_t shift = nb > kBinBits ? nb - kBinBits : 0u;
     for (uint32_t i = tid; i < kBins; i += THREADS) hist[i] = 0u;
     __syncthreads();
-    for (uint32_t i = tid; i < n; i += THREADS) {
-      const uint32_t key = key_at(i);
-      if (key >= lo && key <= hi) atomicAdd(&hist[(key - lo) >> shift], 1u);
+    if (use_list) {
+      for (uint32_t i = tid; i < list_n; i += THREADS) {
+        const uint32_t key = list[i];
+        if (key >= lo && key <= hi) atomicAdd(&hist[(key - lo) >> shift], 1u);
+      }
+    } else {
+      for (uint32_t i = tid; i < n; i += THREADS) {
+        const uint32_t key = key_at(i);
+        if (key >= lo && key <= hi) atomicAdd(&hist[(key - lo) >> shift], 1u);
+      }
     }
     __syncthreads();
     constexpr int BPT = kBins / THREADS;
@@ -181,13 +224,25 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
       }
       scratch[40] = tid * BPT + j;
       scratch[41] = c;
+      scratch[42] = hist[tid * BPT + j];
+      scratch[43] = 0;
     }
     __syncthreads();
     const uint32_t bin = scratch[40];
+    const uint32_t in_bin = scratch[42];
     kk -= scratch[41];
     lo = lo + (bin << shift);
     const uint32_t width = (shift == 0) ? 0u : ((1u << shift) - 1u);
     hi = min(hi, lo + width);
+    if (!use_list && lo != hi && in_bin <= uint32_t(kListCap)) {
+      // the remaining levels only concern the keys of this bin: compact them once (order is irrelevant here)
+      for (uint32_t i = tid; i < n; i += THREADS) {
+        const uint32_t key = key_at(i);
+        if (key >= lo && key <= hi) list[atomicAdd(&scratch[43], 1u)] = key;
+      }
+      use_list = true;
+      list_n = in_bin;
+    }
     __syncthreads();
   }
   const uint32_t T = lo;
@@ -359,7 +414,7 @@ __global__ void zero_two_kernel(uint32_t* a, uint32_t* b) {
 
 template <int THREADS, bool SMEM_KEYS>
 void launch_select_variant(const SelectArgs& args, uint32_t rows, uint32_t n_cap, cudaStream_t stream) {
-  const size_t smem = (size_t(kBins) + 64 + (SMEM_KEYS ? n_cap : 0)) * sizeof(uint32_t);
+  const size_t smem = (size_t(kBins) + 64 + kListCap + args.sel_stride + (SMEM_KEYS ? n_cap : 0)) * sizeof(uint32_t);
   auto kern = select_rows_kernel<THREADS, SMEM_KEYS>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   kern<<<rows, THREADS, smem, stream>>>(args);
@@ -367,8 +422,14 @@ void launch_select_variant(const SelectArgs& args, uint32_t rows, uint32_t n_cap
 
 }  // namespace
 
-int launch_select(const SelectArgs& args, uint32_t rows, uint32_t n_cap, cudaStream_t stream) {
+int launch_select(const SelectArgs& args_in, uint32_t rows, uint32_t n_cap, cudaStream_t stream) {
   if (rows == 0) return 0;
+  SelectArgs args = args_in;
+  args.sel_row_stride = args_in.sel_stride;
+  args.sel_stride = (args_in.mode == kSelCand) ? ((args_in.sel_stride + 3u) & ~3u) : 0u;  // smem words for the block list
+  args.vec_ok = (args.stride % 4 == 0) && (reinterpret_cast<uintptr_t>(args.scores) % 16 == 0) ? 1u : 0u;
+  const uint32_t B = args.block_size;
+  args.block_shift = (B && (B & (B - 1)) == 0) ? uint32_t(__builtin_ctz(B)) : 32u;
   if (n_cap <= 2048) launch_select_variant<128, true>(args, rows, n_cap, stream);
   else if (n_cap <= 16384) launch_select_variant<256, true>(args, rows, n_cap, stream);
   else if (n_cap <= 49152) launch_select_variant<1024, true>(args, rows, n_cap, stream);
