@@ -1,0 +1,69 @@
+#!/usr/bin/env python
+"""Builds the committed profile summaries under profiles/ from the scratch captures in gpurun_out/.
+Usage: python scripts/make_profiles.py r01"""
+import csv
+import json
+import os
+import subprocess
+import sys
+
+tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+out = os.path.join(root, "profiles")
+os.makedirs(out, exist_ok=True)
+
+# 1. launch list: per-kernel share of one bench step (cold-cache, serialised: shares, not absolutes)
+rows = [r for r in csv.reader(open(os.path.join(root, "gpurun_out", "launches.csv"))) if len(r) > 5]
+hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+ix = {h: i for i, h in enumerate(rows[hdr])}
+agg, order = {}, []
+for r in rows[hdr + 1:]:
+    if len(r) != len(rows[hdr]) or r[ix["Metric Name"]] != "gpu__time_duration.sum":
+        continue
+    name = r[ix["Kernel Name"]]
+    val = float(r[ix["Metric Value"]].replace(",", ""))
+    unit = r[ix["Metric Unit"]]
+    ms = val / 1e6 if unit in ("ns", "nsecond") else val / 1e3 if unit in ("us", "usecond") else val
+    if name not in agg:
+        agg[name] = [0, 0.0]
+        order.append(name)
+    agg[name][0] += 1
+    agg[name][1] += ms
+total = sum(v[1] for v in agg.values())
+with open(os.path.join(out, f"{tag}_launches_summary.txt"), "w") as f:
+    f.write("ncu --metrics gpu__time_duration.sum --clock-control none : python bench.py --steps 2 --warmup 1 --flat-steps 1\n")
+    f.write("(3 hisa_select calls + 2 dsa_select calls at C3, L=Q=65536; times are cold-cache and serialised)\n\n")
+    f.write(f"{'kernel':70s} {'launches':>8s} {'total ms':>10s} {'share':>7s}\n")
+    for name in sorted(agg, key=lambda n: -agg[n][1]):
+        f.write(f"{name[:70]:70s} {agg[name][0]:8d} {agg[name][1]:10.3f} {100 * agg[name][1] / total:6.1f}%\n")
+subprocess.run(["cp", os.path.join(root, "gpurun_out", "launches.csv"), os.path.join(out, f"{tag}_launches.csv")], check=True)
+
+# 2. full captures -> short counter tables
+for rep, name in (("prof_score_tc.ncu-rep", "score_tc"), ("prof_select.ncu-rep", "select_rows")):
+    path = os.path.join(root, "gpurun_out", rep)
+    if not os.path.exists(path):
+        continue
+    txt = subprocess.run([sys.executable, os.path.join(root, "scripts", "ncu_summary.py"), path],
+                         capture_output=True, text=True).stdout
+    with open(os.path.join(out, f"{tag}_{name}_ncu_full_summary.txt"), "w") as f:
+        f.write(f"ncu --set full --clock-control none --import-source on -k regex:{name} (python bench.py --steps 1 --warmup 1)\n\n")
+        f.write(txt)
+
+# 3. DRAM traffic of the stage-2 scorer launch -> bench.py's roofline.traffic
+path = os.path.join(root, "gpurun_out", "prof_score_tc.ncu-rep")
+raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rr = list(csv.reader(raw.splitlines()))
+h, units = rr[0], rr[1]
+for r in rr[2:]:
+    d = dict(zip(h, r))
+    if "(int)1, (int)1" in d["Kernel Name"] or "<1, 1" in d["Kernel Name"]:
+        def gb(k):
+            v = float(d[k].replace(",", ""))
+            u = units[h.index(k)]
+            return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[u]
+        rd, wr = gb("dram__bytes_read.sum"), gb("dram__bytes_write.sum")
+        json.dump({"kernel": d["Kernel Name"], "dram_bytes_read": rd, "dram_bytes_write": wr,
+                   "dram_bytes_per_launch": rd + wr, "source": f"profiles/{tag}_score_tc_ncu_full_summary.txt"},
+                  open(os.path.join(out, "traffic_score_tc_stage2.json"), "w"), indent=1)
+        print("stage-2 DRAM traffic per launch: %.3f GB" % ((rd + wr) / 1e9))
+print(open(os.path.join(out, f"{tag}_launches_summary.txt")).read())
