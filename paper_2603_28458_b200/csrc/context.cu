@@ -76,6 +76,14 @@ struct hisa_cuda_ctx {
   uint64_t calls = 0;
 
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+
+  // host-buffer pipeline (select_impl): slices of pipe_rows rows are staged through double-buffered device
+  // arrays so that the H2D copy of slice i+1 and the D2H copy of slice i-1 overlap the kernels of slice i
+  uint32_t pipe_rows = 4096;
+  bool pipe_ready = false;
+  cudaStream_t in_stream = nullptr, out_stream = nullptr;
+  cudaEvent_t ev_in_ready[2]{}, ev_in_free[2]{}, ev_out_ready[2]{}, ev_out_free[2]{};
+  DevBuf st_q[2], st_g[2], st_pos[2], st_idx[2], st_cnt[2], st_cand[2], st_blk[2], st_nblk[2];
 };
 
 namespace {
@@ -436,15 +444,11 @@ void end_call(hisa_cuda_ctx* ctx) {
 
 enum Strategy { kDsa = 0, kHisa = 1, kBlockSparse = 2 };
 
-int select_impl(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const float* gates, const uint32_t* positions,
+// One selection over rows [0, Q): everything is enqueued on ctx->stream. Host pointers are accepted (copied on the
+// same stream, then the stream is synchronised); with device pointers the call returns without synchronising.
+int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const float* gates, const uint32_t* positions,
                 uint64_t Q, int check_finite, int32_t* out_idx, uint32_t* out_count, int32_t* out_blocks,
                 uint32_t* out_nblocks, uint32_t* out_cand) {
-  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
-  if (!out_idx && Q) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "out_idx must be non-null");
-  CU_TRY(ctx, cudaSetDevice(ctx->device));
-  begin_call(ctx);
-  if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "selection over an empty key sequence");
-  if (strat != kDsa) HISA_TRY(ensure_pool(ctx));
   Prepared p;
   HISA_TRY(prepare_inputs(ctx, queries, gates, positions, Q, check_finite, &p));
   if (Q == 0) return HISA_OK;
@@ -612,8 +616,124 @@ int select_impl(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
     if (!cnt_dev) HISA_TRY(copy_out(ctx, out_count ? out_count + q0 : nullptr, cnt_dst, size_t(nq) * 4, &need_sync));
     if (!cand_dev) HISA_TRY(copy_out(ctx, out_cand ? out_cand + q0 : nullptr, cand_dst, size_t(nq) * 4, &need_sync));
   }
-  end_call(ctx);
   if (need_sync) CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return HISA_OK;
+}
+
+int pipe_init(hisa_cuda_ctx* ctx) {
+  if (ctx->pipe_ready) return HISA_OK;
+  CU_TRY(ctx, cudaStreamCreateWithFlags(&ctx->in_stream, cudaStreamNonBlocking));
+  CU_TRY(ctx, cudaStreamCreateWithFlags(&ctx->out_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    CU_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_in_ready[i], cudaEventDisableTiming));
+    CU_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_in_free[i], cudaEventDisableTiming));
+    CU_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_out_ready[i], cudaEventDisableTiming));
+    CU_TRY(ctx, cudaEventCreateWithFlags(&ctx->ev_out_free[i], cudaEventDisableTiming));
+  }
+  ctx->pipe_ready = true;
+  return HISA_OK;
+}
+
+// Host-buffer path: the rows are cut into slices; slice i+1 is copied in (in_stream) and slice i-1 copied out
+// (out_stream) while the kernels of slice i run on ctx->stream. Pointers that already are device memory are
+// passed through untouched.
+int select_pipelined(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const float* gates,
+                     const uint32_t* positions, uint64_t Q, int check_finite, int32_t* out_idx, uint32_t* out_count,
+                     int32_t* out_blocks, uint32_t* out_nblocks, uint32_t* out_cand) {
+  HISA_TRY(pipe_init(ctx));
+  const hisa_cuda_config& c = ctx->cfg;
+  const uint32_t H = c.num_heads, d = c.dim, eb = elem_bytes(ctx);
+  const uint32_t S = c.block_budget + 2;
+  const uint32_t out_width = strat == kBlockSparse ? S * c.block_size : c.token_budget;
+  const bool q_host = !is_device_ptr(queries), g_host = !is_device_ptr(gates), p_host = !is_device_ptr(positions);
+  const bool idx_host = !is_device_ptr(out_idx), cnt_host = out_count && !is_device_ptr(out_count);
+  const bool cand_host = out_cand && !is_device_ptr(out_cand);
+  const bool blk_host = strat != kDsa && out_blocks && !is_device_ptr(out_blocks);
+  const bool nblk_host = strat != kDsa && out_nblocks && !is_device_ptr(out_nblocks);
+  const uint64_t P = ctx->pipe_rows;
+  const size_t q_row = size_t(H) * d * eb;
+  for (int i = 0; i < 2; ++i) {
+    if (q_host) HISA_TRY(ensure(ctx, ctx->st_q[i], P * q_row));
+    if (g_host) HISA_TRY(ensure(ctx, ctx->st_g[i], P * H * sizeof(float)));
+    if (p_host) HISA_TRY(ensure(ctx, ctx->st_pos[i], P * 4));
+    if (idx_host) HISA_TRY(ensure(ctx, ctx->st_idx[i], P * out_width * 4));
+    if (cnt_host) HISA_TRY(ensure(ctx, ctx->st_cnt[i], P * 4));
+    if (cand_host) HISA_TRY(ensure(ctx, ctx->st_cand[i], P * 4));
+    if (blk_host) HISA_TRY(ensure(ctx, ctx->st_blk[i], P * S * 4));
+    if (nblk_host) HISA_TRY(ensure(ctx, ctx->st_nblk[i], P * 4));
+  }
+  const uint64_t nslices = (Q + P - 1) / P;
+  auto copy_in_slice = [&](uint64_t s) -> int {
+    const int b = int(s & 1);
+    const uint64_t q0 = s * P, nq = std::min<uint64_t>(P, Q - q0);
+    if (s >= 2) CU_TRY(ctx, cudaStreamWaitEvent(ctx->in_stream, ctx->ev_in_free[b], 0));
+    if (q_host)
+      CU_TRY(ctx, cudaMemcpyAsync(ctx->st_q[b].p, static_cast<const char*>(queries) + q0 * q_row, nq * q_row,
+                                  cudaMemcpyHostToDevice, ctx->in_stream));
+    if (g_host)
+      CU_TRY(ctx, cudaMemcpyAsync(ctx->st_g[b].p, gates + q0 * H, nq * H * sizeof(float), cudaMemcpyHostToDevice,
+                                  ctx->in_stream));
+    if (p_host)
+      CU_TRY(ctx, cudaMemcpyAsync(ctx->st_pos[b].p, positions + q0, nq * 4, cudaMemcpyHostToDevice, ctx->in_stream));
+    CU_TRY(ctx, cudaEventRecord(ctx->ev_in_ready[b], ctx->in_stream));
+    return HISA_OK;
+  };
+  HISA_TRY(copy_in_slice(0));
+  for (uint64_t s = 0; s < nslices; ++s) {
+    const int b = int(s & 1);
+    const uint64_t q0 = s * P, nq = std::min<uint64_t>(P, Q - q0);
+    if (s + 1 < nslices) HISA_TRY(copy_in_slice(s + 1));
+    CU_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_in_ready[b], 0));
+    if (s >= 2) CU_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_out_free[b], 0));
+    const void* q_s = q_host ? ctx->st_q[b].p : static_cast<const void*>(static_cast<const char*>(queries) + q0 * q_row);
+    const float* g_s = g_host ? ctx->st_g[b].as<float>() : gates + q0 * H;
+    const uint32_t* p_s = p_host ? ctx->st_pos[b].as<uint32_t>() : positions + q0;
+    int32_t* idx_s = idx_host ? ctx->st_idx[b].as<int32_t>() : out_idx + q0 * out_width;
+    uint32_t* cnt_s = !out_count ? nullptr : cnt_host ? ctx->st_cnt[b].as<uint32_t>() : out_count + q0;
+    uint32_t* cand_s = !out_cand ? nullptr : cand_host ? ctx->st_cand[b].as<uint32_t>() : out_cand + q0;
+    int32_t* blk_s = (strat == kDsa || !out_blocks) ? nullptr : blk_host ? ctx->st_blk[b].as<int32_t>() : out_blocks + q0 * S;
+    uint32_t* nblk_s = (strat == kDsa || !out_nblocks) ? nullptr : nblk_host ? ctx->st_nblk[b].as<uint32_t>() : out_nblocks + q0;
+    HISA_TRY(select_core(ctx, strat, q_s, g_s, p_s, nq, check_finite, idx_s, cnt_s, blk_s, nblk_s, cand_s));
+    CU_TRY(ctx, cudaEventRecord(ctx->ev_in_free[b], ctx->stream));
+    CU_TRY(ctx, cudaEventRecord(ctx->ev_out_ready[b], ctx->stream));
+    CU_TRY(ctx, cudaStreamWaitEvent(ctx->out_stream, ctx->ev_out_ready[b], 0));
+    if (idx_host)
+      CU_TRY(ctx, cudaMemcpyAsync(out_idx + q0 * out_width, idx_s, nq * out_width * 4, cudaMemcpyDeviceToHost, ctx->out_stream));
+    if (cnt_host) CU_TRY(ctx, cudaMemcpyAsync(out_count + q0, cnt_s, nq * 4, cudaMemcpyDeviceToHost, ctx->out_stream));
+    if (cand_host) CU_TRY(ctx, cudaMemcpyAsync(out_cand + q0, cand_s, nq * 4, cudaMemcpyDeviceToHost, ctx->out_stream));
+    if (blk_host) CU_TRY(ctx, cudaMemcpyAsync(out_blocks + q0 * S, blk_s, nq * S * 4, cudaMemcpyDeviceToHost, ctx->out_stream));
+    if (nblk_host) CU_TRY(ctx, cudaMemcpyAsync(out_nblocks + q0, nblk_s, nq * 4, cudaMemcpyDeviceToHost, ctx->out_stream));
+    CU_TRY(ctx, cudaEventRecord(ctx->ev_out_free[b], ctx->out_stream));
+  }
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->out_stream));
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return HISA_OK;
+}
+
+int select_impl(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const float* gates, const uint32_t* positions,
+                uint64_t Q, int check_finite, int32_t* out_idx, uint32_t* out_count, int32_t* out_blocks,
+                uint32_t* out_nblocks, uint32_t* out_cand) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  if (!out_idx && Q) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "out_idx must be non-null");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  begin_call(ctx);
+  if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "selection over an empty key sequence");
+  if (strat != kDsa) HISA_TRY(ensure_pool(ctx));
+  if (Q && (!queries || !gates || !positions))
+    return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "queries, gates and positions must be non-null");
+  const bool any_host = Q && (!is_device_ptr(queries) || !is_device_ptr(gates) || !is_device_ptr(positions) ||
+                              !is_device_ptr(out_idx) || (out_count && !is_device_ptr(out_count)) ||
+                              (out_cand && !is_device_ptr(out_cand)) || (out_blocks && !is_device_ptr(out_blocks)) ||
+                              (out_nblocks && !is_device_ptr(out_nblocks)));
+  int rc;
+  if (any_host && ctx->pipe_rows && Q > ctx->pipe_rows)
+    rc = select_pipelined(ctx, strat, queries, gates, positions, Q, check_finite, out_idx, out_count, out_blocks,
+                          out_nblocks, out_cand);
+  else
+    rc = select_core(ctx, strat, queries, gates, positions, Q, check_finite, out_idx, out_count, out_blocks, out_nblocks,
+                     out_cand);
+  HISA_TRY(rc);
+  end_call(ctx);
   return HISA_OK;
 }
 
@@ -753,6 +873,7 @@ int hisa_cuda_create(int device, const hisa_cuda_config* cfg, hisa_cuda_ctx** ou
   ctx->chunk_dense = std::max<uint32_t>(env_u32("HISA_CHUNK_DENSE", 256), 4);
   ctx->chunk_list = std::max<uint32_t>(env_u32("HISA_CHUNK_LIST", 512), 4);
   ctx->workspace_bytes = uint64_t(std::max<uint32_t>(env_u32("HISA_WORKSPACE_MB", 4096), 16)) << 20;
+  ctx->pipe_rows = env_u32("HISA_PIPE_ROWS", 4096);  // 0 disables the host-buffer pipeline
   *out = ctx;
   return HISA_OK;
 }
@@ -766,6 +887,18 @@ int hisa_cuda_destroy(hisa_cuda_ctx* ctx) {
                     &ctx->scalars, &ctx->cand, &ctx->flat, &ctx->out_idx, &ctx->out_count, &ctx->out_cand,
                     &ctx->generic_scores, &ctx->generic_n, &ctx->export_a, &ctx->export_b, &ctx->flag, &ctx->stats})
     release(*b);
+  for (int i = 0; i < 2; ++i)
+    for (DevBuf* b : {&ctx->st_q[i], &ctx->st_g[i], &ctx->st_pos[i], &ctx->st_idx[i], &ctx->st_cnt[i], &ctx->st_cand[i],
+                      &ctx->st_blk[i], &ctx->st_nblk[i]})
+      release(*b);
+  if (ctx->pipe_ready) {
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(ctx->ev_in_ready[i]); cudaEventDestroy(ctx->ev_in_free[i]);
+      cudaEventDestroy(ctx->ev_out_ready[i]); cudaEventDestroy(ctx->ev_out_free[i]);
+    }
+    cudaStreamDestroy(ctx->in_stream);
+    cudaStreamDestroy(ctx->out_stream);
+  }
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->stream);
   delete ctx;

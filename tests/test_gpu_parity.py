@@ -379,3 +379,26 @@ def test_error_behaviour():
         assert e.value.name == "ShapeMismatch"
         r = ix.hisa_select(q, w, np.uint32([8]))                      # position == L is a streaming query
         assert r["count"][0] == 4
+
+
+# ------------------------------------------------------------------------------------------ host-buffer pipeline
+@pytest.mark.parametrize("strategy", ["hisa", "dsa", "block"])
+def test_host_buffer_pipeline_equals_single_pass(oracle, strategy, monkeypatch):
+    """Host buffers are staged slice by slice (H2D of slice i+1 and D2H of slice i-1 overlap the kernels of
+    slice i). The sliced result must equal the unsliced one bit for bit, ragged last slice included."""
+    L, H, d, B, m, k = 1500, 64, 128, 64, 4, 128
+    pos = np.arange(L, dtype=np.uint32)
+    prob = oracle.make_inputs("random", 5, L, pos, H, d, block_size=B, block_budget=m, token_budget=k)
+    q, kk = round_problem_to_bf16(prob)
+    res = {}
+    for rows in (0, 192):
+        monkeypatch.setenv("HISA_PIPE_ROWS", str(rows))
+        with indexer_for(prob) as ix:
+            ix.upload_keys(kk)
+            ix.pool_build()
+            res[rows] = ix._select(strategy, q, prob.gates, pos)
+    for key in ("idx", "count") + (("blocks", "nblocks") if strategy != "dsa" else ()) + (("cand",) if strategy != "block" else ()):
+        assert np.array_equal(res[0][key], res[192][key]), key
+    sample = np.arange(0, L, 37)
+    _, _, rec = compare_selection(oracle, prob, strategy, res[192], sample, BF16_RTOL)
+    assert rec >= 0.999
