@@ -101,6 +101,7 @@ struct SelectArgs {
   uint32_t sel_stride;      // entries per row of `sel` (launch_select turns it into the smem word count)
   uint32_t sel_row_stride;  // filled by launch_select: row stride of `sel` in global memory
   uint32_t vec_ok;          // filled by launch_select: score rows are 16-byte aligned
+  uint32_t vec_out;         // filled by launch_select: output rows are 16-byte aligned
   uint32_t block_shift;     // filled by launch_select: log2(block_size) or 32
   uint32_t tie_break, force_first_last, forced_in_budget;
   int32_t* out_idx;  // [rows, out_stride], -1 padded

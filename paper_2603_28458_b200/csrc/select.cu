@@ -15,6 +15,9 @@
 // candidate_union (hisa/hisa.hpp:30-33) never materialises: stage-2 candidates are addressed as
 // (slot, offset) inside the row's selected-block list and mapped to token positions on output.
 #include "kernels.cuh"
+#include "ptx.cuh"
+
+#include <cstdlib>
 
 namespace hisa_dev {
 
@@ -291,6 +294,456 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------------
+// Warp-per-row selection for short rows (n_cap <= 32 * KPL): select_blocks at prefill sizes (<= 512 blocks)
+// and small top-k problems. Keys live in registers (element i = lane + 32 j); the keep-th largest key is found
+// by a bitwise radix descent that starts at the highest bit in which min and max differ (one warp-wide
+// REDUX per bit), and the ordered compaction uses ballots. No shared memory, no block barriers.
+// ---------------------------------------------------------------------------------------------------
+constexpr int kWarpSelThreads = 256;
+
+template <int KPL>
+__global__ void __launch_bounds__(kWarpSelThreads) select_warp_kernel(SelectArgs a, uint32_t rows) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t row = blockIdx.x * (kWarpSelThreads / 32) + (threadIdx.x >> 5);
+  if (row >= rows) return;  // warp-uniform
+  constexpr uint32_t FULL = 0xffffffffu;
+  const bool block_mode = (a.mode == kSelBlocks || a.mode == kSelBlocksGeneric);
+  const uint32_t B = a.block_size;
+  uint32_t n = 0;
+  const int32_t* sel_row = nullptr;
+  if (a.mode == kSelFlat) {
+    n = min(a.pos[row], a.seq_len - 1) + 1;
+  } else if (a.mode == kSelBlocks) {
+    n = min(min(a.pos[row], a.seq_len - 1) / B, a.num_blocks - 1) + 1;
+  } else if (a.mode == kSelCand) {
+    const uint32_t t = min(a.pos[row], a.seq_len - 1);
+    const uint32_t ns = a.nsel[row];
+    sel_row = a.sel + uint64_t(row) * a.sel_row_stride;
+    const uint32_t lastb = uint32_t(sel_row[ns - 1]);
+    n = (ns - 1) * B + min(B, t - lastb * B + 1);
+  } else {
+    n = a.n_in[row];
+  }
+  const float* srow = a.scores + uint64_t(row) * a.stride;
+  int32_t* orow = a.out_idx + uint64_t(row) * a.out_stride;
+  const uint32_t keep = a.keep;
+  const bool forced = block_mode && a.force_first_last && n > 0;
+  const uint32_t bshift = a.block_shift;
+  auto position_of = [&](uint32_t i) -> int32_t {
+    if (a.mode == kSelCand) {
+      const uint32_t slot = bshift < 32 ? i >> bshift : i / B;
+      return int32_t(uint32_t(sel_row[slot]) * B + (i - slot * B));
+    }
+    return int32_t(i);
+  };
+  if (a.out_cand && lane == 0) a.out_cand[row] = n;
+  if (n <= keep) {  // dense regime
+    for (uint32_t i = lane; i < a.out_width; i += 32) orow[i] = i < n ? position_of(i) : -1;
+    if (a.out_count && lane == 0) a.out_count[row] = n;
+    return;
+  }
+  const bool boost = forced && a.forced_in_budget;
+  uint32_t key[KPL];
+  uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    const uint32_t i = lane + 32u * j;
+    uint32_t k = 0u;  // 0 = not a candidate (no finite score maps to key 0)
+    if (i < n) {
+      k = score_key(srow[i]);
+      if (boost && (i == 0 || i == n - 1)) k = 0xFFFFFFFFu;
+      kmin = min(kmin, k);
+      kmax = max(kmax, k);
+    }
+    key[j] = k;
+  }
+  const uint32_t lo = __reduce_min_sync(FULL, kmin), hi = __reduce_max_sync(FULL, kmax);
+  uint32_t T = hi, kk = keep;
+  if (lo != hi) {
+    const int top = 31 - __clz(lo ^ hi);
+    uint32_t prefix = hi & ~((2u << top) - 1u);  // bits above `top` are common to all candidates
+    for (int bit = top; bit >= 0; --bit) {
+      const uint32_t want = (prefix >> bit) | 1u;
+      uint32_t c = 0;
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) c += ((key[j] >> bit) == want) ? 1u : 0u;
+      c = __reduce_add_sync(FULL, c);
+      if (c >= kk) prefix |= 1u << bit;
+      else kk -= c;
+    }
+    T = prefix;
+  }
+  const uint32_t need = kk;  // ties (key == T) to take
+  uint32_t cG = 0, cE = 0;
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    cG += key[j] > T;
+    cE += key[j] == T;
+  }
+  const uint32_t totG = __reduce_add_sync(FULL, cG), totE = __reduce_add_sync(FULL, cE);
+  const uint32_t skip = a.tie_break ? totE - need : 0u;
+  uint32_t add_first = 0, add_last = 0;
+  if (forced) {
+    const uint32_t k0 = __shfl_sync(FULL, key[0], 0);
+    uint32_t kl_local = 0;
+#pragma unroll
+    for (int j = 0; j < KPL; ++j)
+      if (lane + 32u * j == n - 1) kl_local = key[j];
+    const uint32_t kl = __reduce_max_sync(FULL, kl_local);
+    const bool sel0 = k0 > T || (k0 == T && skip == 0);
+    const bool sell = kl > T || (kl == T && (totE - 1 >= skip) && (totE - 1 < skip + need));
+    add_first = sel0 ? 0u : 1u;
+    add_last = sell ? 0u : 1u;
+  }
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t o_run = add_first, e_run = 0;
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    if (32u * j >= n) break;  // warp-uniform
+    const bool g = key[j] > T, e = key[j] == T;
+    const uint32_t be = __ballot_sync(FULL, e);
+    const uint32_t erank = e_run + __popc(be & lt);
+    const bool emit = g || (e && erank >= skip && erank < skip + need);
+    const uint32_t bm = __ballot_sync(FULL, emit);
+    if (emit) orow[o_run + __popc(bm & lt)] = position_of(lane + 32u * j);
+    o_run += __popc(bm);
+    e_run += __popc(be);
+  }
+  const uint32_t count = totG + need + add_first + add_last;
+  if (lane == 0) {
+    if (add_first) orow[0] = position_of(0);
+    if (add_last) orow[count - 1] = position_of(n - 1);
+    if (a.out_count) a.out_count[row] = count;
+  }
+  for (uint32_t i = count + lane; i < a.out_width; i += 32) orow[i] = -1;
+}
+
+// ---------------------------------------------------------------------------------------------------
+// CTA-per-row selection for medium rows (n_cap <= THREADS * PER4 * 4; the stage-2 candidate pool of
+// (m+2)*B = 8448 scores is the case it is sized for). Same result as select_rows_kernel, built for fewer
+// instructions and barriers per row:
+//   * the score row arrives by ONE bulk copy (cp.async.bulk -> mbarrier), no register staging;
+//   * every pass over the keys is 128-bit (LDS.128), strided for the histogram passes, blocked (each thread
+//     owns PER4*4 consecutive keys; PER4 odd keeps the 128-bit accesses conflict-free) for the ordered output;
+//   * after the first 11-bit range-adaptive level the few survivors are ranked directly (all-pairs count),
+//     which replaces the two remaining radix levels in the common case;
+//   * one packed block scan (greater | equal << 16) instead of two; ties only take the slow per-key path
+//     when the threshold value really is shared;
+//   * indices are staged in shared memory (the dead histogram) and leave as coalesced 128-bit stores
+//     together with the -1 padding.
+// ---------------------------------------------------------------------------------------------------
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_scan_excl_packed(uint32_t v, uint32_t* wsum, uint32_t& total) {
+  // wsum: THREADS/32 words, must not be in use by a previous call without an intervening barrier
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  uint32_t before = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < THREADS / 32; ++w) {
+    const uint32_t x = wsum[w];
+    before += w < warp ? x : 0u;
+    tot += x;
+  }
+  total = tot;
+  return before + inc - v;
+}
+
+template <int THREADS, int PER4>
+__global__ void __launch_bounds__(THREADS) select_cta_kernel(SelectArgs a) {
+  constexpr uint32_t CAP = THREADS * PER4 * 4;
+  constexpr uint32_t CAP4 = CAP / 4;
+  constexpr int NW = THREADS / 32;
+  extern __shared__ __align__(16) uint32_t smem_u[];
+  uint32_t* skey = smem_u;                   // [CAP] scores, then keys
+  uint32_t* hist = skey + CAP;               // [kBins]; reused as the index staging [<= kBins]
+  uint32_t* list = hist + kBins;             // [kListCap]
+  uint32_t* ssel = list + kListCap;          // [sel_stride]
+  uint32_t* scratch = ssel + a.sel_stride;   // [96]
+  __shared__ __align__(8) uint64_t bar;
+
+  const uint32_t row = blockIdx.x;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t lane = tid & 31u;
+  const bool block_mode = (a.mode == kSelBlocks || a.mode == kSelBlocksGeneric);
+  const uint32_t B = a.block_size;
+
+  uint32_t n = 0;
+  const int32_t* sel_row = nullptr;
+  uint32_t ns = 0;
+  if (a.mode == kSelFlat) {
+    n = min(a.pos[row], a.seq_len - 1) + 1;
+  } else if (a.mode == kSelBlocks) {
+    n = min(min(a.pos[row], a.seq_len - 1) / B, a.num_blocks - 1) + 1;
+  } else if (a.mode == kSelCand) {
+    const uint32_t t = min(a.pos[row], a.seq_len - 1);
+    ns = a.nsel[row];
+    sel_row = a.sel + uint64_t(row) * a.sel_row_stride;
+    const uint32_t lastb = uint32_t(sel_row[ns - 1]);
+    n = (ns - 1) * B + min(B, t - lastb * B + 1);
+  } else {
+    n = a.n_in[row];
+  }
+  const float* srow = a.scores + uint64_t(row) * a.stride;
+  int32_t* orow = a.out_idx + uint64_t(row) * a.out_stride;
+  const uint32_t keep = a.keep;
+  const bool forced = block_mode && a.force_first_last && n > 0;
+  const uint32_t bshift = a.block_shift;
+  auto position_of = [&](uint32_t i) -> int32_t {
+    if (a.mode == kSelCand) {
+      const uint32_t slot = bshift < 32 ? i >> bshift : i / B;
+      return int32_t(ssel[slot] * B + (i - slot * B));
+    }
+    return int32_t(i);
+  };
+  if (a.out_cand && tid == 0) a.out_cand[row] = n;
+
+  const bool dense = n <= keep;
+  const uint32_t n4 = (n + 3u) >> 2;  // 16-byte chunks that hold candidates
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+    if (!dense) {
+      mbar_arrive_expect_tx(&bar, n4 * 16u);
+      bulk_load_1d(skey, srow, n4 * 16u, &bar);  // may read up to 3 floats past n: still inside the row's stride
+    }
+    scratch[0] = 0xFFFFFFFFu;  // min key
+    scratch[1] = 0u;           // max key
+    scratch[2] = 0u;           // list fill
+  }
+  for (uint32_t i = tid; i < ns; i += THREADS) ssel[i] = uint32_t(sel_row[i]);
+  for (uint32_t i = tid; i < kBins / 4; i += THREADS) reinterpret_cast<uint4*>(hist)[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+
+  if (dense) {  // everything fits
+    for (uint32_t i = tid; i < a.out_width; i += THREADS) orow[i] = i < n ? position_of(i) : -1;
+    if (a.out_count && tid == 0) a.out_count[row] = n;
+    return;
+  }
+  mbar_wait(&bar, 0);
+
+  // ---- scores -> keys in place, min / max ------------------------------------------------------------
+  const bool boost = forced && a.forced_in_budget;
+  uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+  for (uint32_t c = tid; c < CAP4; c += THREADS) {
+    uint4 kq = make_uint4(0u, 0u, 0u, 0u);  // 0 = not a candidate (no finite score maps to key 0)
+    if (c < n4) {
+      const float4 v = reinterpret_cast<const float4*>(skey)[c];
+      const uint32_t i0 = c << 2;
+      kq.x = score_key(v.x);
+      kq.y = i0 + 1 < n ? score_key(v.y) : 0u;
+      kq.z = i0 + 2 < n ? score_key(v.z) : 0u;
+      kq.w = i0 + 3 < n ? score_key(v.w) : 0u;
+      if (boost) {
+        if (i0 == 0) kq.x = 0xFFFFFFFFu;
+        if (i0 == ((n - 1) & ~3u)) {
+          const uint32_t e = (n - 1) & 3u;
+          if (e == 0) kq.x = 0xFFFFFFFFu; else if (e == 1) kq.y = 0xFFFFFFFFu; else if (e == 2) kq.z = 0xFFFFFFFFu; else kq.w = 0xFFFFFFFFu;
+        }
+      }
+      kmax = max(max(kmax, kq.x), max(max(kq.y, kq.z), kq.w));
+      kmin = min(kmin, kq.x);
+      if (kq.y) kmin = min(kmin, kq.y);
+      if (kq.z) kmin = min(kmin, kq.z);
+      if (kq.w) kmin = min(kmin, kq.w);
+    }
+    reinterpret_cast<uint4*>(skey)[c] = kq;
+  }
+  kmin = __reduce_min_sync(0xffffffffu, kmin);
+  kmax = __reduce_max_sync(0xffffffffu, kmax);
+  if (lane == 0) {
+    atomicMin(&scratch[0], kmin);
+    atomicMax(&scratch[1], kmax);
+  }
+  __syncthreads();
+  uint32_t lo = scratch[0], hi = scratch[1];
+
+  // ---- threshold: range-adaptive radix levels, finished by direct ranking of the survivors -------------
+  uint32_t kk = keep;
+  bool use_list = false;
+  uint32_t list_n = 0;
+  uint32_t T = 0, need = 0;
+  bool done = false;
+  uint32_t* wsum = scratch + 8;  // [NW] x 2, alternating so consecutive scans need no extra barrier
+  uint32_t scan_flip = 0;
+  while (!done) {
+    if (lo == hi) {
+      T = lo;
+      need = kk;
+      break;
+    }
+    if (use_list && list_n <= uint32_t(THREADS)) {
+      // rank the survivors directly: the kk-th largest of the list is the threshold
+      uint32_t mine = 0, g = 0, e = 0;
+      if (tid < list_n) {
+        mine = list[tid];
+        for (uint32_t j = 0; j < list_n; ++j) {
+          const uint32_t other = list[j];
+          g += other > mine;
+          e += other == mine;
+        }
+        if (g < kk && kk <= g + e) {  // all threads holding this value write the same words
+          scratch[4] = mine;
+          scratch[5] = kk - g;
+        }
+      }
+      __syncthreads();
+      T = scratch[4];
+      need = scratch[5];
+      break;
+    }
+    const uint32_t range = hi - lo;
+    const uint32_t nb = 32 - __clz(range);
+    const uint32_t shift = nb > kBinBits ? nb - kBinBits : 0u;
+    if (use_list) {
+      for (uint32_t i = tid; i < list_n; i += THREADS) {
+        const uint32_t key = list[i];
+        if (key >= lo && key <= hi) atomicAdd(&hist[(key - lo) >> shift], 1u);
+      }
+    } else {
+      for (uint32_t c = tid; c < n4; c += THREADS) {
+        const uint4 kq = reinterpret_cast<const uint4*>(skey)[c];
+        if (kq.x >= lo && kq.x <= hi) atomicAdd(&hist[(kq.x - lo) >> shift], 1u);
+        if (kq.y >= lo && kq.y <= hi) atomicAdd(&hist[(kq.y - lo) >> shift], 1u);
+        if (kq.z >= lo && kq.z <= hi) atomicAdd(&hist[(kq.z - lo) >> shift], 1u);
+        if (kq.w >= lo && kq.w <= hi) atomicAdd(&hist[(kq.w - lo) >> shift], 1u);
+      }
+    }
+    __syncthreads();
+    constexpr int BPT = kBins / THREADS;
+    uint32_t hb[BPT];
+    uint32_t loc = 0;
+#pragma unroll
+    for (int j = 0; j < BPT; ++j) {
+      hb[j] = hist[tid * BPT + j];
+      loc += hb[j];
+    }
+    uint32_t total;
+    const uint32_t before = block_scan_excl_packed<THREADS>(loc, wsum + scan_flip * NW, total);
+    scan_flip ^= 1u;
+    const uint32_t above = total - before - loc;  // keys in bins owned by higher threads
+    if (above < kk && kk <= above + loc) {
+      uint32_t c = above;
+      int j = BPT - 1;
+#pragma unroll
+      for (int jj = BPT - 1; jj > 0; --jj) {
+        if (j == jj && c + hb[jj] < kk) {
+          c += hb[jj];
+          j = jj - 1;
+        }
+      }
+      scratch[40] = tid * BPT + j;
+      scratch[41] = c;
+      scratch[42] = hb[j];
+    }
+    __syncthreads();
+    const uint32_t bin = scratch[40];
+    const uint32_t in_bin = scratch[42];
+    kk -= scratch[41];
+    lo = lo + (bin << shift);
+    const uint32_t width = (shift == 0) ? 0u : ((1u << shift) - 1u);
+    hi = min(hi, lo + width);
+    if (lo == hi) continue;  // exits at the top of the loop
+    if (!use_list && in_bin <= uint32_t(kListCap)) {
+      // the remaining work only concerns the keys of this bin: compact them once (order is irrelevant here)
+      for (uint32_t c = tid; c < n4; c += THREADS) {
+        const uint4 kq = reinterpret_cast<const uint4*>(skey)[c];
+        if (kq.x >= lo && kq.x <= hi) list[atomicAdd(&scratch[2], 1u)] = kq.x;
+        if (kq.y >= lo && kq.y <= hi) list[atomicAdd(&scratch[2], 1u)] = kq.y;
+        if (kq.z >= lo && kq.z <= hi) list[atomicAdd(&scratch[2], 1u)] = kq.z;
+        if (kq.w >= lo && kq.w <= hi) list[atomicAdd(&scratch[2], 1u)] = kq.w;
+      }
+      use_list = true;
+      list_n = in_bin;
+      if (list_n > uint32_t(THREADS))
+        for (uint32_t i = tid; i < kBins / 4; i += THREADS) reinterpret_cast<uint4*>(hist)[i] = make_uint4(0u, 0u, 0u, 0u);
+    } else {
+      for (uint32_t i = tid; i < kBins / 4; i += THREADS) reinterpret_cast<uint4*>(hist)[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    __syncthreads();
+  }
+
+  // ---- ordered compaction: each thread owns PER4*4 consecutive keys ----------------------------------------
+  uint4 kq[PER4];
+  uint32_t cG = 0, cE = 0;
+#pragma unroll
+  for (int j = 0; j < PER4; ++j) {
+    kq[j] = reinterpret_cast<const uint4*>(skey)[tid * PER4 + j];
+    cG += (kq[j].x > T) + (kq[j].y > T) + (kq[j].z > T) + (kq[j].w > T);
+    cE += (kq[j].x == T) + (kq[j].y == T) + (kq[j].z == T) + (kq[j].w == T);
+  }
+  uint32_t tot;
+  const uint32_t pre = block_scan_excl_packed<THREADS>(cG | (cE << 16), wsum + scan_flip * NW, tot);
+  const uint32_t totG = tot & 0xFFFFu, totE = tot >> 16;
+  const uint32_t gBefore = pre & 0xFFFFu, eBefore = pre >> 16;
+  const uint32_t skip = a.tie_break ? totE - need : 0u;
+  uint32_t add_first = 0, add_last = 0;
+  if (forced) {
+    const uint32_t k0 = skey[0], kl = skey[n - 1];
+    const bool sel0 = k0 > T || (k0 == T && skip == 0);
+    const bool sell = kl > T || (kl == T && (totE - 1 >= skip) && (totE - 1 < skip + need));
+    add_first = sel0 ? 0u : 1u;
+    add_last = sell ? 0u : 1u;
+  }
+  const uint32_t count = totG + need + add_first + add_last;
+  const bool staged = count <= uint32_t(kBins);  // the histogram is dead: stage the indices there
+  const uint32_t tiesBefore = eBefore > skip ? min(eBefore - skip, need) : 0u;
+  uint32_t o = gBefore + tiesBefore + add_first;
+  uint32_t e = eBefore;
+  const bool all_ties = need == totE;
+  auto put = [&](uint32_t where, int32_t v) {
+    if (staged) hist[where] = uint32_t(v);
+    else orow[where] = v;
+  };
+#pragma unroll
+  for (int j = 0; j < PER4; ++j) {
+    const uint32_t i0 = (tid * PER4 + j) << 2;
+    const uint32_t ks[4] = {kq[j].x, kq[j].y, kq[j].z, kq[j].w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t key = ks[u];
+      bool emit = key > T;
+      if (key == T) {
+        emit = all_ties || ((e >= skip) && (e < skip + need));
+        ++e;
+      }
+      if (emit) put(o++, position_of(i0 + u));
+    }
+  }
+  if (tid == 0) {
+    if (add_first) put(0, position_of(0));
+    if (add_last) put(count - 1, position_of(n - 1));
+    if (a.out_count) a.out_count[row] = count;
+  }
+  if (staged) {
+    __syncthreads();
+    if (a.vec_out) {
+      const uint32_t w4 = a.out_width >> 2;
+      for (uint32_t c = tid; c < w4; c += THREADS) {
+        const uint32_t i0 = c << 2;
+        int4 v;
+        v.x = i0 + 0 < count ? int32_t(hist[i0 + 0]) : -1;
+        v.y = i0 + 1 < count ? int32_t(hist[i0 + 1]) : -1;
+        v.z = i0 + 2 < count ? int32_t(hist[i0 + 2]) : -1;
+        v.w = i0 + 3 < count ? int32_t(hist[i0 + 3]) : -1;
+        reinterpret_cast<int4*>(orow)[c] = v;
+      }
+      for (uint32_t i = (w4 << 2) + tid; i < a.out_width; i += THREADS) orow[i] = i < count ? int32_t(hist[i]) : -1;
+    } else {
+      for (uint32_t i = tid; i < a.out_width; i += THREADS) orow[i] = i < count ? int32_t(hist[i]) : -1;
+    }
+  } else {
+    for (uint32_t i = count + tid; i < a.out_width; i += THREADS) orow[i] = -1;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------------
 // dense work list (stage 1 and the flat indexer): chunk-major items, only tiles a chunk can need.
 // ---------------------------------------------------------------------------------------------------
 constexpr int kDenseThreads = 1024;
@@ -412,6 +865,24 @@ __global__ void zero_two_kernel(uint32_t* a, uint32_t* b) {
   *b = 0;
 }
 
+template <int KPL>
+void launch_select_warp(const SelectArgs& args, uint32_t rows, cudaStream_t stream) {
+  const uint32_t per_cta = kWarpSelThreads / 32;
+  select_warp_kernel<KPL><<<(rows + per_cta - 1) / per_cta, kWarpSelThreads, 0, stream>>>(args, rows);
+}
+
+template <int THREADS, int PER4>
+void launch_select_cta(const SelectArgs& args, uint32_t rows, cudaStream_t stream) {
+  const size_t smem = (size_t(THREADS) * PER4 * 4 + kBins + kListCap + args.sel_stride + 96) * sizeof(uint32_t);
+  auto kern = select_cta_kernel<THREADS, PER4>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  kern<<<rows, THREADS, smem, stream>>>(args);
+}
+
 template <int THREADS, bool SMEM_KEYS>
 void launch_select_variant(const SelectArgs& args, uint32_t rows, uint32_t n_cap, cudaStream_t stream) {
   const size_t smem = (size_t(kBins) + 64 + kListCap + args.sel_stride + (SMEM_KEYS ? n_cap : 0)) * sizeof(uint32_t);
@@ -430,7 +901,17 @@ int launch_select(const SelectArgs& args_in, uint32_t rows, uint32_t n_cap, cuda
   args.vec_ok = (args.stride % 4 == 0) && (reinterpret_cast<uintptr_t>(args.scores) % 16 == 0) ? 1u : 0u;
   const uint32_t B = args.block_size;
   args.block_shift = (B && (B & (B - 1)) == 0) ? uint32_t(__builtin_ctz(B)) : 32u;
-  if (n_cap <= 2048) launch_select_variant<128, true>(args, rows, n_cap, stream);
+  args.vec_out = (args.out_stride % 4 == 0) && (reinterpret_cast<uintptr_t>(args.out_idx) % 16 == 0) ? 1u : 0u;
+  const bool legacy = getenv("HISA_SELECT_LEGACY") != nullptr;  // cross-check switch for the tests
+  // bulk-copy path: 16-byte aligned rows whose stride covers the rounded-up chunk count
+  const bool bulk_ok = args.vec_ok && args.scores != nullptr;
+  if (!legacy && n_cap <= 128) launch_select_warp<4>(args, rows, stream);
+  else if (!legacy && n_cap <= 512) launch_select_warp<16>(args, rows, stream);
+  else if (!legacy && n_cap <= 1024) launch_select_warp<32>(args, rows, stream);
+  else if (!legacy && bulk_ok && n_cap <= 256 * 9 * 4) launch_select_cta<256, 9>(args, rows, stream);
+  else if (!legacy && bulk_ok && n_cap <= 512 * 9 * 4) launch_select_cta<512, 9>(args, rows, stream);
+  else if (!legacy && bulk_ok && n_cap <= 1024 * 9 * 4) launch_select_cta<1024, 9>(args, rows, stream);
+  else if (n_cap <= 2048) launch_select_variant<128, true>(args, rows, n_cap, stream);
   else if (n_cap <= 16384) launch_select_variant<256, true>(args, rows, n_cap, stream);
   else if (n_cap <= 49152) launch_select_variant<1024, true>(args, rows, n_cap, stream);
   else launch_select_variant<1024, false>(args, rows, n_cap, stream);
