@@ -277,7 +277,13 @@ def run_b200(a, rank, world, local_rank):
     stalls = {}
     for st_name, st in stages["stalls"].items():
         cta = max(st["cta"], 1)
-        stalls[st_name] = {kk: (round(vv / cta, 4) if kk != "groups" else vv) for kk, vv in st.items() if kk != "cta"}
+        stalls[st_name] = {kk: (round(vv / cta, 4) if kk != "groups" else vv) for kk, vv in st.items()
+                           if kk != "cta" and not kk.startswith("epi_")}
+        # SM clock the kernel really ran at: CTA lifetime cycles (one persistent CTA per SM) / its CUDA-event time
+        st_ms = stages["score_blocks_ms" if st_name == "stage1" else "score_tokens_ms"]
+        if st_ms > 0:
+            n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+            stalls[st_name]["sm_mhz_in_kernel"] = round(st["cta"] / n_sm / (st_ms * 1e-3) / 1e6, 1)
 
     # ---- in-run comparison: the flat DSA indexer built from the same kernels
     flat = None

@@ -23,9 +23,9 @@ constexpr int kDim = 128;       // elements per operand segment (padded d)
 constexpr int kGroupQ = 4;      // queries per MMA group (UMMA N = 256)
 constexpr int kMaxSeg = 3;
 
-// position of head j inside a query's 64-float gate row: heads {8r + 2c, 8r + 2c + 1 : r = 0..7} are the columns
-// that tcgen05.ld.16x256b hands to the lanes with (lane % 4) == c, and are stored as 16 consecutive floats.
-__host__ __device__ constexpr uint32_t gate_slot(uint32_t j) { return ((j % 8) / 2) * 16 + (j / 8) * 2 + (j % 2); }
+// position of head j inside a query's 64-float gate row: heads {4i + c : i = 0..15} are the columns that
+// tcgen05.ld.16x128b hands to the lanes with (lane % 4) == c, and are stored as 16 consecutive floats.
+__host__ __device__ constexpr uint32_t gate_slot(uint32_t j) { return (j % 4) * 16 + j / 4; }
 
 // One unit of scorer work: one operand tile against `count` queries.
 //   dense mode: queries are rows first .. first+count-1, results go to out[row, tile*128 + lane]

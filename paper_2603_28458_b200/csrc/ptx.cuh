@@ -72,6 +72,42 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
   }
 }
+// shared-space address variants: keep the hot loops free of generic->shared conversions
+__device__ __forceinline__ bool mbar_try_wait_addr(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t parity) {
+  if (mbar_try_wait_addr(bar, parity)) return;
+  const uint64_t t0 = global_timer_ns();
+  uint32_t spins = 0;
+  while (!mbar_try_wait_addr(bar, parity)) {
+    if ((++spins & 0xFFu) == 0 && global_timer_ns() - t0 > HISA_MBAR_TIMEOUT_NS) {
+      printf("hisa: mbarrier wait timed out (block %d thread %d bar 0x%x parity %u)\n", blockIdx.x, threadIdx.x, bar,
+             parity);
+      asm volatile("trap;");
+    }
+  }
+}
+__device__ __forceinline__ void mbar_arrive_addr(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// register re-partitioning between warp groups (all warps of a 4-warp group must execute the same one)
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
 // same, adding the cycles spent waiting to `acc` (role-level stall accounting, see ScoreArgs::stats)
 // (try_wait itself suspends for a while, so the clock is read around the whole wait)
 __device__ __forceinline__ void mbar_wait_timed(uint64_t* bar, uint32_t parity, uint64_t& acc) {
@@ -79,9 +115,20 @@ __device__ __forceinline__ void mbar_wait_timed(uint64_t* bar, uint32_t parity, 
   mbar_wait(bar, parity);
   acc += uint64_t(clock64() - c0);
 }
+// 32-bit variant for warps that are short of registers (sums stay below 2^32 cycles for any launch under 2 s)
+__device__ __forceinline__ void mbar_wait_timed32(uint64_t* bar, uint32_t parity, uint32_t& acc) {
+  const uint32_t c0 = uint32_t(clock());
+  mbar_wait(bar, parity);
+  acc += uint32_t(clock()) - c0;
+}
 __device__ __forceinline__ float4 lds_f4(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint2 lds_u2(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
@@ -189,12 +236,12 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)
       : "memory");
 }
 
-// 16 lanes x 64 consecutive fp32 columns (8 x 256 bit). Thread T of the warp receives, for every group i of 8
-// columns: r[4i+0], r[4i+1] = (lane base + T/4,     columns 8i + 2(T%4), +1)
-//          r[4i+2], r[4i+3] = (lane base + T/4 + 8, columns 8i + 2(T%4), +1)
-__device__ __forceinline__ void tmem_ld_16x256b_x8(uint32_t taddr, uint32_t (&r)[32]) {
+// 16 lanes x 64 consecutive fp32 columns (16 x 128 bit). Thread T of the warp receives, for every group i of 4
+// columns: r[2i] = (lane base + T/4, column 4i + T%4), r[2i+1] = (lane base + T/4 + 8, column 4i + T%4).
+// Measured on B200 (tools/tmem_ld_bench.cu): 505 B/clk/SM, against 254 for 16x256b and 866 for 32x32b.
+__device__ __forceinline__ void tmem_ld_16x128b_x16(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.16x256b.x8.b32 "
+      "tcgen05.ld.sync.aligned.16x128b.x16.b32 "
       "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
       "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),

@@ -28,9 +28,10 @@
 //     the issuing thread keeps up, so the issue loop is written to be lean: warp-uniform control flow (all
 //     lanes wait, one elected lane issues), descriptors built by adding constants to per-stage bases.
 //
-// Warp roles (608 threads): warps 0-15 epilogue (warp%4 = TMEM lane quarter, warp/4 = which of the 4 queries;
-// four epilogue warps per SM sub-partition hide the TMEM-load and LDS latencies of each other), warp 16 TMA
-// producer, warp 17 MMA issuer + TMEM owner, warp 18 scheduler.
+// Warp roles (352 threads): warps 0-7 epilogue (warp%4 = TMEM lane quarter, warp/4 = which PAIR of the 4 queries),
+// warp 8 TMA producer, warp 9 MMA issuer + TMEM owner, warp 10 scheduler. Eight fat epilogue warps (up to 184
+// registers) instead of sixteen thin ones: the fixed per-group cost of an epilogue warp (barrier wait, meta reads,
+// output address, shuffles) is paid half as often, and each warp keeps a tcgen05.ld in flight under its own math.
 #include "kernels.cuh"
 #include "ptx.cuh"
 
@@ -38,11 +39,11 @@ namespace hisa_dev {
 
 namespace {
 
-constexpr int kEpiWarps = 16;
-constexpr int kProducerWarp = 16;
-constexpr int kMmaWarp = 17;
-constexpr int kSchedWarp = 18;
-constexpr int kTcThreads = 19 * 32;
+constexpr int kEpiWarps = 8;
+constexpr int kProducerWarp = 8;
+constexpr int kMmaWarp = 9;
+constexpr int kSchedWarp = 10;
+constexpr int kTcThreads = 11 * 32;
 constexpr int kMetaSlots = 8;
 constexpr int kUnitSlots = 4;
 constexpr uint32_t kAHalfBytes = kTileRows * 128;      // one 64-element K-half of one A segment: 16 KB
@@ -94,25 +95,50 @@ __device__ __forceinline__ void ffma2(float2& acc, float a0, float a1, float b0,
   asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(cv));
 }
 
-// gate * relu head reduction over two tcgen05.ld.16x256b.x8 fragments (see ptx.cuh): this lane holds heads
-// {8i + 2c, 8i + 2c + 1 : i = 0..7} of four key rows (two per fragment) and reads its 16 permuted gates with
-// 4 x LDS.128; each gate pair feeds four packed FMAs, so only a few gate registers are live at a time.
-__device__ __forceinline__ void reduce_fragments(const uint32_t (&va)[32], const uint32_t (&vb)[32], uint32_t waddr,
-                                                 float2& a0, float2& a1, float2& a2, float2& a3) {
+// gate * relu head reduction over part of ONE tcgen05.ld.16x128b.x16 fragment (see ptx.cuh): the lane holds heads
+// {4i + c : i = 0..15} of two key rows; gw[] are its 16 permuted gates (4 x LDS.128, loaded once per query and used
+// for both halves). PART selects heads i in [8 PART, 8 PART + 8): each gate pair feeds two packed FMAs, one per row.
+template <int PART>
+__device__ __forceinline__ void reduce_part(const uint32_t (&v)[32], const float4 (&gw)[4], float2& a0, float2& a1) {
 #pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    const float4 w4 = waddr ? lds_f4(waddr + h * 16) : make_float4(1.f, 1.f, 1.f, 1.f);
+  for (int h = 2 * PART; h < 2 * PART + 2; ++h) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const int i = 2 * h + e;
-      const float wx = e ? w4.z : w4.x, wy = e ? w4.w : w4.y;
-      ffma2(a0, wx, wy, fmaxf(__uint_as_float(va[4 * i + 0]), 0.f), fmaxf(__uint_as_float(va[4 * i + 1]), 0.f));
-      ffma2(a1, wx, wy, fmaxf(__uint_as_float(va[4 * i + 2]), 0.f), fmaxf(__uint_as_float(va[4 * i + 3]), 0.f));
-      ffma2(a2, wx, wy, fmaxf(__uint_as_float(vb[4 * i + 0]), 0.f), fmaxf(__uint_as_float(vb[4 * i + 1]), 0.f));
-      ffma2(a3, wx, wy, fmaxf(__uint_as_float(vb[4 * i + 2]), 0.f), fmaxf(__uint_as_float(vb[4 * i + 3]), 0.f));
+      const int i = 2 * h + e;  // heads 8i + c and 8i + 4 + c
+      const float wx = e ? gw[h].z : gw[h].x, wy = e ? gw[h].w : gw[h].y;
+      ffma2(a0, wx, wy, fmaxf(__uint_as_float(v[4 * i + 0]), 0.f), fmaxf(__uint_as_float(v[4 * i + 2]), 0.f));
+      ffma2(a1, wx, wy, fmaxf(__uint_as_float(v[4 * i + 1]), 0.f), fmaxf(__uint_as_float(v[4 * i + 3]), 0.f));
     }
   }
 }
+__device__ __forceinline__ void load_gates(float4 (&gw)[4], uint32_t waddr) {
+#pragma unroll
+  for (int h = 0; h < 4; ++h) gw[h] = lds_f4(waddr + h * 16);
+}
+
+// Transposed butterfly over the 4 lanes that share key rows: each lane enters with its partial sums of four rows and
+// leaves with the full sum of row slot (lane & 3). Split into three steps so that the two shuffle latencies can be
+// covered by the reduction of the next half-fragment.
+struct RowSum {
+  float keep0, keep1, got0, got1;
+  float* dst;
+  bool ok;
+  __device__ __forceinline__ void step1(const float2& a0, const float2& a1, const float2& a2, const float2& a3, bool b0) {
+    const float s0 = a0.x + a0.y, s1 = a1.x + a1.y, s2 = a2.x + a2.y, s3 = a3.x + a3.y;
+    keep0 = b0 ? s1 : s0;
+    keep1 = b0 ? s3 : s2;
+    got0 = __shfl_xor_sync(0xffffffffu, b0 ? s0 : s1, 1);
+    got1 = __shfl_xor_sync(0xffffffffu, b0 ? s2 : s3, 1);
+  }
+  __device__ __forceinline__ void step2(bool b1) {
+    const float k0 = keep0 + got0, k1 = keep1 + got1;
+    keep0 = b1 ? k1 : k0;
+    got0 = __shfl_xor_sync(0xffffffffu, b1 ? k0 : k1, 2);
+  }
+  __device__ __forceinline__ void step3() {
+    if (ok) *dst = keep0 + got0;
+  }
+};
 
 // TERMS: bit (ib * 3 + ia) set <=> A segment ia is multiplied with B segment ib
 template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST>
@@ -314,11 +340,19 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       mbar_wait_timed(&b_full[stage], sph, st_bf);
       const uint32_t word = lds_u32(meta_base + ws * uint32_t(sizeof(GroupMeta)) + 32);
       const uint32_t flags = (word >> 8) & 0xFFu;
-      if (flags & kFlagTerminate) break;
+      const uint32_t acc = g & 1u;
+      if (flags & kFlagTerminate) {
+        // the epilogue only watches t_full: pass the terminate marker on through it
+        mbar_wait(&t_empty[acc], ((g >> 1) & 1u) ^ 1u);
+        if (lane == 0) mbar_arrive(&t_full[acc]);
+        break;
+      }
       const uint32_t nvalid = word & 0xFFu;
       const uint32_t a_buf = units % ABUF;  // same sequence as the producer's useq % ABUF
       if (flags & kFlagFirst) mbar_wait_timed(&a_full[a_buf], (units / ABUF) & 1u, st_af);
-      const uint32_t acc = g & 1u;
+      // gates of the group have landed (issued before its first query chunk): t_full then covers them as well, and
+      // the epilogue warps wait on a single barrier per group
+      mbar_wait_timed(&w_full[ws], (g / kMetaSlots) & 1u, st_bf);
       mbar_wait_timed(&t_empty[acc], ((g >> 1) & 1u) ^ 1u, st_te);
       __syncwarp();
       tc_fence_after();
@@ -368,62 +402,105 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       atomicAdd(a.stats + kStatMmaTEmpty, st_te);
       atomicAdd(a.stats + kStatGroups, (unsigned long long)g);
     }
-  } else {
+  } else if (warp < kEpiWarps) {
     // ================= epilogue: TMEM -> gate*ReLU head reduction -> HBM =================
+    // Each warp reduces a 32-row quarter of the tile for TWO queries of the group = four half-fragments of 32
+    // registers (tcgen05.ld.16x128b.x16), software-pipelined through two register buffers: the load of the next half
+    // is in flight while the FMNMX/FFMA2 work of the current one issues, and the last half of group g is reduced
+    // under the first load of group g+1 (the accumulator is handed back as soon as all four loads have landed).
+    // Fragment layout (tcgen05.ld.16x128b, twice the TMEM read rate of 16x256b): a lane owns 16 of the 64 heads for two key rows per half, so it needs
+    // only 16 gates (64 B) per query instead of all 64: the gate traffic through the 128 B/clk shared-memory return
+    // path is what bounded a one-row-per-thread (32x32b) epilogue. The 4 lanes sharing a row are summed by shuffles.
     const uint32_t quarter = warp & 3u;
-    const uint32_t qi = warp >> 2;  // which query of the group this warp reduces
-    const uint32_t w_base = smem_u32(s_w);
-    uint64_t st_w = 0, st_t = 0, st_busy = 0;
+    const uint32_t qp = (warp >> 2) * 2u;  // first of the two queries this warp reduces
+    const uint32_t w_lane = smem_u32(s_w) + qp * kGateRowBytes + (lane & 3u) * 64u;
+    const uint32_t t_lane = tmem_base + ((quarter * 32u) << 16) + qp * kHeads;
+    const uint32_t row = quarter * 32 + (lane >> 2) + 8u * (lane & 3u);
+    const bool b0 = lane & 1u, b1 = lane & 2u;
+    const uint32_t t_full_addr = smem_u32(t_full), t_empty_addr = smem_u32(t_empty);
+    uint32_t va[32], vb[32];
+    float4 g0[4], g1[4];                         // gates of the warp's two queries (this lane's 16 heads each)
+    float2 c0 = make_float2(0.f, 0.f), c1 = c0;  // first-half sums of the deferred (second) query
+    bool pend = false;                           // its second half (in vb) still has to be reduced and stored
+    RowSum f0, f1;
+    f0.ok = f1.ok = false;
+    f0.dst = f1.dst = nullptr;
     for (uint32_t g = 0;; ++g) {
       const uint32_t ws = g % kMetaSlots;
-      mbar_wait_timed(&w_full[ws], (g / kMetaSlots) & 1u, st_w);
+      const uint32_t acc = g & 1u;
+      mbar_wait_addr(t_full_addr + acc * 8, (g >> 1) & 1u);
       const uint32_t maddr = meta_base + ws * uint32_t(sizeof(GroupMeta));
       const uint32_t word = lds_u32(maddr + 32);
       if ((word >> 8) & kFlagTerminate) break;
       const uint32_t nvalid = word & 0xFFu;
-      const uint32_t valid_rows = word >> 16;
-      const uint32_t acc = g & 1u;
-      mbar_wait_timed(&t_full[acc], (g >> 1) & 1u, st_t);
-      const long long c0 = clock64();
-      __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the spin loops
+      const bool row_ok = row < (word >> 16);
+      __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the spin loop
       tc_fence_after();
-      const bool active = qi < nvalid && !(a.debug_flags & 1u);
-      // Fragment layout (tcgen05.ld.16x256b): a lane owns 16 of the 64 heads for FOUR key rows, so it needs only
-      // 16 gates (64 B) per query instead of all 64: the gate traffic through the 128 B/clk shared-memory port
-      // is what bounded the 32x32b one-row-per-thread epilogue. The 4 lanes sharing a row are summed by shuffles.
-      uint32_t v0[32], v1[32];
-      if (active) {
-        const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * kAccCols + qi * kHeads;
-        tmem_ld_16x256b_x8(taddr, v0);               // rows quarter*32 + {T/4, T/4 + 8}
-        tmem_ld_16x256b_x8(taddr + (16u << 16), v1);  // rows quarter*32 + 16 + {T/4, T/4 + 8}
-        tmem_ld_wait();
+      const bool act0 = qp < nvalid && !(a.debug_flags & 1u);
+      const bool act1 = qp + 1 < nvalid && !(a.debug_flags & 1u);
+      const uint32_t taddr = t_lane + acc * kAccCols;
+      const uint32_t waddr = w_lane + ws * (kGroupQ * kGateRowBytes);
+      if (act0) {
+        tmem_ld_16x128b_x16(taddr, va);  // query 0, rows quarter*32 + {T/4, T/4 + 8}
+        load_gates(g0, waddr);
       }
-      // the dots are in registers: hand the accumulator back before doing the math
+      float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+      if (pend) {  // previous group's last half (query 1, rows + 16), under the load just issued
+        reduce_part<0>(vb, g1, a2, a3);
+        reduce_part<1>(vb, g1, a2, a3);
+        f1.step1(c0, c1, a2, a3, b0);
+        a2 = a3 = make_float2(0.f, 0.f);
+      }
+      if (act0) {
+        const uint2 qrows = lds_u2(maddr + qp * 4), qcols = lds_u2(maddr + 16 + qp * 4);
+        tmem_ld_wait();
+        tmem_ld_16x128b_x16(taddr + (16u << 16), vb);  // query 0, rows + 16
+        reduce_part<0>(va, g0, a0, a1);
+        if (pend) f1.step2(b1);
+        reduce_part<1>(va, g0, a0, a1);
+        if (pend) f1.step3();
+        tmem_ld_wait();
+        if (act1) {
+          tmem_ld_16x128b_x16(taddr + kHeads, va);  // query 1, first half
+          load_gates(g1, waddr + kGateRowBytes);
+        }
+        reduce_part<0>(vb, g0, a2, a3);
+        reduce_part<1>(vb, g0, a2, a3);
+        f0.dst = a.out + uint64_t(qrows.x) * a.out_stride + qcols.x + row;
+        f0.ok = row_ok;
+        f0.step1(a0, a1, a2, a3, b0);
+        if (act1) {
+          tmem_ld_wait();
+          tmem_ld_16x128b_x16(taddr + kHeads + (16u << 16), vb);  // query 1, rows + 16: reduced in the next iteration
+          c0 = c1 = make_float2(0.f, 0.f);
+          reduce_part<0>(va, g1, c0, c1);
+          f0.step2(b1);
+          reduce_part<1>(va, g1, c0, c1);
+          f0.step3();
+          tmem_ld_wait();
+          f1.dst = a.out + uint64_t(qrows.y) * a.out_stride + qcols.y + row;
+          f1.ok = row_ok;
+        } else {
+          f0.step2(b1);
+          f0.step3();
+        }
+      } else if (pend) {
+        f1.step2(b1);
+        f1.step3();
+      }
+      // all dots of the group are in registers: hand the accumulator back to the MMA warp
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&t_empty[acc]);
-      if (active && !(a.debug_flags & 8u)) {  // (debug 8: loads only, debug 16: no gate loads)
-        const uint32_t waddr = (a.debug_flags & 16u) ? 0u : w_base + (ws * kGroupQ + qi) * kGateRowBytes + (lane & 3u) * 64u;
-        float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
-        reduce_fragments(v0, v1, waddr, a0, a1, a2, a3);
-        const float s0 = a0.x + a0.y, s1 = a1.x + a1.y, s2 = a2.x + a2.y, s3 = a3.x + a3.y;
-        // transposed butterfly over the 4 lanes of a row group: lane ends with the total of row slot (lane & 3)
-        const bool b0 = lane & 1u, b1 = lane & 2u;
-        float k0 = b0 ? s1 : s0, k1 = b0 ? s3 : s2;
-        k0 += __shfl_xor_sync(0xffffffffu, b0 ? s0 : s1, 1);
-        k1 += __shfl_xor_sync(0xffffffffu, b0 ? s2 : s3, 1);
-        float z = b1 ? k1 : k0;
-        z += __shfl_xor_sync(0xffffffffu, b1 ? k0 : k1, 2);
-        const uint32_t row = quarter * 32 + (lane >> 2) + 8u * (lane & 3u);
-        if (row < valid_rows)
-          a.out[uint64_t(lds_u32(maddr + qi * 4)) * a.out_stride + lds_u32(maddr + 16 + qi * 4) + row] = z;
-      }
-      st_busy += uint64_t(clock64() - c0);
+      if (lane == 0) mbar_arrive_addr(t_empty_addr + acc * 8);
+      pend = act1;
     }
-    if (a.stats && warp == 0 && lane == 0) {
-      atomicAdd(a.stats + kStatEpiWFull, st_w);
-      atomicAdd(a.stats + kStatEpiTFull, st_t);
-      atomicAdd(a.stats + kStatEpiBusy, st_busy);
+    if (pend) {
+      float2 a2 = make_float2(0.f, 0.f), a3 = a2;
+      reduce_part<0>(vb, g1, a2, a3);
+      reduce_part<1>(vb, g1, a2, a3);
+      f1.step1(c0, c1, a2, a3, b0);
+      f1.step2(b1);
+      f1.step3();
     }
   }
 

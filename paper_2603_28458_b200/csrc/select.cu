@@ -744,6 +744,324 @@ __global__ void __launch_bounds__(THREADS) select_cta_kernel(SelectArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------------
+// CTA-per-row top-k over token candidates with the keys held in REGISTERS (modes kSelFlat / kSelCand /
+// kSelGeneric, n_cap <= THREADS * PER4 * 4; sized for the stage-2 pool of (m+2)*B = 8448 scores, k = 2048).
+// select_cta_kernel re-read its shared-memory keys in every pass and spent ~85 thread-instructions per key;
+// this kernel touches shared memory once per key (blocked LDS.128: thread t owns keys [36 t, 36 t + 36)) and
+// every later pass is register arithmetic:
+//   * histogram level: key - lo, one unsigned compare (also rejects the zero keys of non-candidates), shift,
+//     RED.shared;
+//   * levels repeat on the registers until the threshold bin holds <= THREADS keys, which are compacted and
+//     ranked all-pairs: that yields the threshold T, how many keys equal to T are kept, and how many exist;
+//   * ordered output: one bit per key (key >= T when every tie is kept, the common case), popc + one block scan,
+//     then a loop over the SET bits only; a thread's 36 consecutive candidates span at most two selected blocks,
+//     so their token positions are idx + one of two per-thread deltas;
+//   * indices are staged in the dead histogram and leave as coalesced 128-bit stores with the -1 padding.
+// ---------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t score_key_fast(float f) {
+  const uint32_t b = __float_as_uint(f + 0.0f);  // -0 + +0 = +0: both zeros share a key
+  return b ^ (uint32_t(int32_t(b) >> 31) | 0x80000000u);
+}
+
+template <int THREADS, int PER4>
+__global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
+  constexpr int KPT = PER4 * 4;
+  constexpr uint32_t CAP = THREADS * KPT;
+  constexpr int NW = THREADS / 32;
+  constexpr int BPT = kBins / THREADS;
+  static_assert(KPT > 32 && KPT <= 64, "two 32-bit emit masks per thread");
+  static_assert(BPT % 4 == 0, "each thread owns whole 16-byte groups of histogram bins");
+  extern __shared__ __align__(16) uint32_t smem_u[];
+  uint32_t* skey = smem_u;                  // [CAP] scores as delivered by the bulk copy
+  uint32_t* hist = skey + CAP;              // [kBins]; reused as the index staging
+  uint32_t* list = hist + kBins;            // [THREADS] survivors of the last radix level
+  uint32_t* ssel = list + THREADS;          // [sel_stride]
+  uint32_t* scratch = ssel + a.sel_stride;  // [96]
+  __shared__ __align__(8) uint64_t bar;
+
+  const uint32_t row = blockIdx.x;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t lane = tid & 31u;
+  const uint32_t B = a.block_size;
+  const bool cand = a.mode == kSelCand;
+
+  uint32_t n = 0, ns = 0;
+  const int32_t* sel_row = nullptr;
+  if (a.mode == kSelFlat) {
+    n = min(a.pos[row], a.seq_len - 1) + 1;
+  } else if (cand) {
+    const uint32_t t = min(a.pos[row], a.seq_len - 1);
+    ns = a.nsel[row];
+    sel_row = a.sel + uint64_t(row) * a.sel_row_stride;
+    const uint32_t lastb = uint32_t(sel_row[ns - 1]);
+    n = (ns - 1) * B + min(B, t - lastb * B + 1);
+  } else {
+    n = a.n_in[row];
+  }
+  const float* srow = a.scores + uint64_t(row) * a.stride;
+  int32_t* orow = a.out_idx + uint64_t(row) * a.out_stride;
+  const uint32_t keep = a.keep;
+  const uint32_t bshift = a.block_shift;
+  auto position_of = [&](uint32_t i) -> int32_t {
+    if (cand) {
+      const uint32_t slot = bshift < 32 ? i >> bshift : i / B;
+      return int32_t(ssel[slot] * B + (i - slot * B));
+    }
+    return int32_t(i);
+  };
+  if (a.out_cand && tid == 0) a.out_cand[row] = n;
+
+  const bool dense = n <= keep;
+  const uint32_t n4 = (n + 3u) >> 2;  // 16-byte chunks that hold candidates
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+    if (!dense) {
+      mbar_arrive_expect_tx(&bar, n4 * 16u);
+      bulk_load_1d(skey, srow, n4 * 16u, &bar);  // may read up to 3 floats past n: still inside the row's stride
+    }
+    scratch[0] = 0xFFFFFFFFu;  // min key
+    scratch[1] = 0u;           // max key
+    scratch[2] = 0u;           // list fill
+  }
+  for (uint32_t i = tid; i < ns; i += THREADS) ssel[i] = uint32_t(sel_row[i]);
+#pragma unroll
+  for (int j = 0; j < BPT / 4; ++j) reinterpret_cast<uint4*>(hist)[tid * (BPT / 4) + j] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+
+  if (dense) {  // everything fits
+    for (uint32_t i = tid; i < a.out_width; i += THREADS) orow[i] = i < n ? position_of(i) : -1;
+    if (a.out_count && tid == 0) a.out_count[row] = n;
+    return;
+  }
+  mbar_wait(&bar, 0);
+
+  // ---- scores -> keys in registers (0 = not a candidate: no finite score maps to key 0), min / max ------
+  uint32_t k[KPT];
+  const uint32_t first = tid * KPT;
+  {
+    const uint32_t c0 = tid * PER4;
+#pragma unroll
+    for (int j = 0; j < PER4; ++j) {
+      // chunks past the copied range hold stale shared memory: never read them as scores
+      const float4 v = c0 + j < n4 ? reinterpret_cast<const float4*>(skey)[c0 + j] : make_float4(0.f, 0.f, 0.f, 0.f);
+      k[4 * j + 0] = score_key_fast(v.x);
+      k[4 * j + 1] = score_key_fast(v.y);
+      k[4 * j + 2] = score_key_fast(v.z);
+      k[4 * j + 3] = score_key_fast(v.w);
+    }
+  }
+  uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+  if (first + KPT <= n) {
+#pragma unroll
+    for (int e = 0; e < KPT; ++e) {
+      kmin = min(kmin, k[e]);
+      kmax = max(kmax, k[e]);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < KPT; ++e) {
+      if (first + e >= n) k[e] = 0u;
+      if (k[e]) kmin = min(kmin, k[e]);
+      kmax = max(kmax, k[e]);
+    }
+  }
+  kmin = __reduce_min_sync(0xffffffffu, kmin);
+  kmax = __reduce_max_sync(0xffffffffu, kmax);
+  if (lane == 0) {
+    atomicMin(&scratch[0], kmin);
+    atomicMax(&scratch[1], kmax);
+  }
+  __syncthreads();
+  uint32_t lo = scratch[0], hi = scratch[1];
+
+  // ---- threshold: range-adaptive radix levels on the registers, finished by ranking the survivors -------
+  uint32_t kk = keep;        // rank of the threshold among the keys still in [lo, hi]
+  uint32_t in_range = n;     // number of keys in [lo, hi]
+  uint32_t T = 0, need = 0, totE = 0;
+  uint32_t* wsum = scratch + 8;  // [NW] x 2, alternating so consecutive scans need no extra barrier
+  uint32_t scan_flip = 0;
+  for (;;) {
+    if (lo == hi) {  // every remaining key is the threshold value
+      T = lo;
+      need = kk;
+      totE = in_range;
+      break;
+    }
+    const uint32_t span = hi - lo;
+    if (in_range <= uint32_t(THREADS)) {
+      // compact the keys of the threshold range (order is irrelevant) and rank them all-pairs
+#pragma unroll
+      for (int e = 0; e < KPT; ++e)
+        if (k[e] - lo <= span) list[atomicAdd(&scratch[2], 1u)] = k[e];
+      __syncthreads();
+      if (tid < in_range) {
+        const uint32_t mine = list[tid];
+        uint32_t g = 0, eq = 0;
+        for (uint32_t j = 0; j < in_range; ++j) {
+          const uint32_t other = list[j];
+          g += other > mine;
+          eq += other == mine;
+        }
+        if (g < kk && kk <= g + eq) {  // all threads holding this value write the same words
+          scratch[4] = mine;
+          scratch[5] = kk - g;
+          scratch[6] = eq;
+        }
+      }
+      __syncthreads();
+      T = scratch[4];
+      need = scratch[5];
+      totE = scratch[6];
+      break;
+    }
+    const uint32_t nb = 32 - __clz(span);
+    const uint32_t shift = nb > kBinBits ? nb - kBinBits : 0u;
+#pragma unroll
+    for (int e = 0; e < KPT; ++e) {
+      const uint32_t dlt = k[e] - lo;  // zero keys wrap around to a huge value (lo > 0)
+      if (dlt <= span) atomicAdd(&hist[dlt >> shift], 1u);
+    }
+    __syncthreads();
+    uint32_t hb[BPT];
+    uint32_t loc = 0;
+    {
+      const uint4* h4 = reinterpret_cast<const uint4*>(hist) + tid * (BPT / 4);
+#pragma unroll
+      for (int j = 0; j < BPT / 4; ++j) {
+        const uint4 h = h4[j];
+        hb[4 * j + 0] = h.x; hb[4 * j + 1] = h.y; hb[4 * j + 2] = h.z; hb[4 * j + 3] = h.w;
+        loc += h.x + h.y + h.z + h.w;
+      }
+    }
+    uint32_t total;
+    const uint32_t before = block_scan_excl_packed<THREADS>(loc, wsum + scan_flip * NW, total);
+    scan_flip ^= 1u;
+    const uint32_t above = total - before - loc;  // keys in bins owned by higher threads
+    if (above < kk && kk <= above + loc) {
+      uint32_t c = above;
+      int j = BPT - 1;
+#pragma unroll
+      for (int jj = BPT - 1; jj > 0; --jj) {
+        if (j == jj && c + hb[jj] < kk) {
+          c += hb[jj];
+          j = jj - 1;
+        }
+      }
+      scratch[40] = tid * BPT + j;
+      scratch[41] = c;
+      scratch[42] = hb[j];
+    }
+    // the histogram words this thread owns are dead now: clear them for the next level / keep them clean
+#pragma unroll
+    for (int j = 0; j < BPT / 4; ++j) reinterpret_cast<uint4*>(hist)[tid * (BPT / 4) + j] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    const uint32_t bin = scratch[40];
+    in_range = scratch[42];
+    kk -= scratch[41];
+    lo = lo + (bin << shift);
+    const uint32_t width = (shift == 0) ? 0u : ((1u << shift) - 1u);
+    hi = min(hi, lo + width);
+  }
+
+  // ---- ordered output -------------------------------------------------------------------------------------
+  // bit e of (m0, m1) <=> key e of this thread is emitted
+  uint32_t m0 = 0, m1 = 0;
+  const bool all_ties = need == totE;
+  uint32_t cE = 0;
+  if (all_ties) {
+#pragma unroll
+    for (int e = 0; e < KPT; ++e) {
+      if (k[e] >= T) {
+        if (e < 32) m0 |= 1u << e; else m1 |= 1u << (e - 32);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < KPT; ++e) {
+      if (k[e] > T) {
+        if (e < 32) m0 |= 1u << e; else m1 |= 1u << (e - 32);
+      }
+      cE += k[e] == T;
+    }
+  }
+  uint32_t tot;
+  uint32_t pre = block_scan_excl_packed<THREADS>((__popc(m0) + __popc(m1)) | (cE << 16), wsum + scan_flip * NW, tot);
+  scan_flip ^= 1u;
+  uint32_t o = pre & 0xFFFFu;
+  if (!all_ties) {
+    // only `need` of the totE keys equal to T are kept: the first ones (SmallestIndex) or the last ones
+    const uint32_t skip = a.tie_break ? totE - need : 0u;
+    uint32_t eidx = pre >> 16;
+    o += eidx > skip ? min(eidx - skip, need) : 0u;
+#pragma unroll
+    for (int e = 0; e < KPT; ++e) {
+      if (k[e] == T) {
+        if (eidx >= skip && eidx < skip + need) {
+          if (e < 32) m0 |= 1u << e; else m1 |= 1u << (e - 32);
+        }
+        ++eidx;
+      }
+    }
+  }
+  const uint32_t count = keep;  // n > keep here, so exactly `keep` candidates are selected
+  const bool staged = count <= uint32_t(kBins);  // the histogram is dead: stage the indices there
+  // candidate mode: the thread's KPT consecutive candidates lie in at most two selected blocks when B >= KPT
+  int32_t delta0 = 0, delta1 = 0;
+  uint32_t boundary = 0xFFFFFFFFu;
+  const bool two_block = cand && bshift < 32 && B >= uint32_t(KPT);
+  if (two_block) {
+    const uint32_t slot0 = first >> bshift;
+    boundary = (slot0 + 1) << bshift;
+    delta0 = slot0 < ns ? int32_t((ssel[slot0] - slot0) << bshift) : 0;
+    delta1 = slot0 + 1 < ns ? int32_t((ssel[slot0 + 1] - (slot0 + 1)) << bshift) : 0;
+  }
+  auto emit = [&](uint32_t idx) {
+    int32_t v;
+    if (two_block) v = int32_t(idx) + (idx < boundary ? delta0 : delta1);
+    else v = position_of(idx);
+    if (staged) hist[o] = uint32_t(v);
+    else orow[o] = v;
+    ++o;
+  };
+  while (m0) {
+    const uint32_t e = __ffs(m0) - 1;
+    m0 &= m0 - 1;
+    emit(first + e);
+  }
+  while (m1) {
+    const uint32_t e = __ffs(m1) - 1;
+    m1 &= m1 - 1;
+    emit(first + 32 + e);
+  }
+  if (tid == 0 && a.out_count) a.out_count[row] = count;
+  if (staged) {
+    __syncthreads();
+    if (a.vec_out) {
+      const uint32_t w4 = a.out_width >> 2;
+      for (uint32_t c = tid; c < w4; c += THREADS) {
+        const uint32_t i0 = c << 2;
+        int4 v;
+        if (i0 + 3 < count) {
+          v = reinterpret_cast<const int4*>(hist)[c];
+        } else {
+          v.x = i0 + 0 < count ? int32_t(hist[i0 + 0]) : -1;
+          v.y = i0 + 1 < count ? int32_t(hist[i0 + 1]) : -1;
+          v.z = i0 + 2 < count ? int32_t(hist[i0 + 2]) : -1;
+          v.w = i0 + 3 < count ? int32_t(hist[i0 + 3]) : -1;
+        }
+        reinterpret_cast<int4*>(orow)[c] = v;
+      }
+      for (uint32_t i = (w4 << 2) + tid; i < a.out_width; i += THREADS) orow[i] = i < count ? int32_t(hist[i]) : -1;
+    } else {
+      for (uint32_t i = tid; i < a.out_width; i += THREADS) orow[i] = i < count ? int32_t(hist[i]) : -1;
+    }
+  } else {
+    for (uint32_t i = count + tid; i < a.out_width; i += THREADS) orow[i] = -1;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------------
 // dense work list (stage 1 and the flat indexer): chunk-major items, only tiles a chunk can need.
 // ---------------------------------------------------------------------------------------------------
 constexpr int kDenseThreads = 1024;
@@ -883,6 +1201,18 @@ void launch_select_cta(const SelectArgs& args, uint32_t rows, cudaStream_t strea
   kern<<<rows, THREADS, smem, stream>>>(args);
 }
 
+template <int THREADS, int PER4>
+void launch_select_tok(const SelectArgs& args, uint32_t rows, cudaStream_t stream) {
+  const size_t smem = (size_t(THREADS) * PER4 * 4 + kBins + THREADS + args.sel_stride + 96) * sizeof(uint32_t);
+  auto kern = select_tok_kernel<THREADS, PER4>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  kern<<<rows, THREADS, smem, stream>>>(args);
+}
+
 template <int THREADS, bool SMEM_KEYS>
 void launch_select_variant(const SelectArgs& args, uint32_t rows, uint32_t n_cap, cudaStream_t stream) {
   const size_t smem = (size_t(kBins) + 64 + kListCap + args.sel_stride + (SMEM_KEYS ? n_cap : 0)) * sizeof(uint32_t);
@@ -902,12 +1232,16 @@ int launch_select(const SelectArgs& args_in, uint32_t rows, uint32_t n_cap, cuda
   const uint32_t B = args.block_size;
   args.block_shift = (B && (B & (B - 1)) == 0) ? uint32_t(__builtin_ctz(B)) : 32u;
   args.vec_out = (args.out_stride % 4 == 0) && (reinterpret_cast<uintptr_t>(args.out_idx) % 16 == 0) ? 1u : 0u;
-  const bool legacy = getenv("HISA_SELECT_LEGACY") != nullptr;  // cross-check switch for the tests
+  const bool legacy = getenv("HISA_SELECT_LEGACY") != nullptr;  // cross-check switches for the tests
+  const bool cta_old = getenv("HISA_SELECT_CTA_SMEM") != nullptr;
+  const bool block_mode = args.mode == kSelBlocks || args.mode == kSelBlocksGeneric;
   // bulk-copy path: 16-byte aligned rows whose stride covers the rounded-up chunk count
   const bool bulk_ok = args.vec_ok && args.scores != nullptr;
   if (!legacy && n_cap <= 128) launch_select_warp<4>(args, rows, stream);
   else if (!legacy && n_cap <= 512) launch_select_warp<16>(args, rows, stream);
   else if (!legacy && n_cap <= 1024) launch_select_warp<32>(args, rows, stream);
+  else if (!legacy && bulk_ok && !block_mode && !cta_old && n_cap <= 256 * 9 * 4) launch_select_tok<256, 9>(args, rows, stream);
+  else if (!legacy && bulk_ok && !block_mode && !cta_old && n_cap <= 512 * 9 * 4) launch_select_tok<512, 9>(args, rows, stream);
   else if (!legacy && bulk_ok && n_cap <= 256 * 9 * 4) launch_select_cta<256, 9>(args, rows, stream);
   else if (!legacy && bulk_ok && n_cap <= 512 * 9 * 4) launch_select_cta<512, 9>(args, rows, stream);
   else if (!legacy && bulk_ok && n_cap <= 1024 * 9 * 4) launch_select_cta<1024, 9>(args, rows, stream);
