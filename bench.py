@@ -42,12 +42,15 @@ def parse_args():
     ap.add_argument("--cpu-rows", type=int, default=768, help="rows of the workload the CPU baseline is timed on")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp8"],
+                    help="storage of q/k: bf16 (headline) or e4m3 with per-token key scales (query scales folded into the gates)")
     return ap.parse_args()
 
 
 def workload_name(a):
+    store = "bf16 q/k" if a.dtype == "bf16" else "e4m3 q/k + f32 per-key scales"
     return (f"C3 prefill L=Q={a.seq_len} H=64 d=128 B={a.block_size} m={a.block_budget} k={a.token_budget} "
-            f"bf16 q/k, fp32 gates, hisa_select")
+            f"{store}, fp32 gates, hisa_select")
 
 
 def load_peaks():
@@ -179,14 +182,32 @@ def run_b200(a, rank, world, local_rank):
     g.manual_seed(a.seed)
     # keys: generated on rank 0 and replicated (NCCL broadcast over NVLink); queries: each rank generates only
     # the rows it owns (synthetic, so nothing has to be scattered)
-    keys = torch.randn((L, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    fp8 = a.dtype == "fp8"
+    keys = torch.randn((L, d), generator=g, device=dev, dtype=torch.float32)
+    key_scales = None
+    if fp8:  # per-token symmetric quantisation (synthetic-input plumbing; the product consumes bytes + scales)
+        key_scales = (keys.abs().amax(dim=1) / 448.0).clamp_min(1e-12).contiguous()
+        keys = (keys / key_scales[:, None]).to(torch.float8_e4m3fn)
+    else:
+        keys = keys.to(torch.bfloat16)
     if dist:
-        dist.broadcast(keys, src=0)
+        dist.broadcast(keys.view(torch.uint8) if fp8 else keys, src=0)
+        if fp8:
+            dist.broadcast(key_scales, src=0)
     rows = rank_rows(Q, world, rank)
     nq = len(rows)
     g.manual_seed(a.seed + 1000 + rank)
-    q = torch.randn((nq, H, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
     w = torch.rand((nq, H), generator=g, device=dev, dtype=torch.float32) + 0.5
+    if fp8:
+        q = torch.empty((nq, H, d), device=dev, dtype=torch.float8_e4m3fn)
+        for r0 in range(0, nq, 8192):  # quantise in slices: the f32 staging of all of q would be 2 GiB
+            qf = torch.randn((min(8192, nq - r0), H, d), generator=g, device=dev, dtype=torch.float32)
+            qs = (qf.abs().amax(dim=2) / 448.0).clamp_min(1e-12)
+            q[r0:r0 + qf.shape[0]] = (qf / qs[:, :, None]).to(torch.float8_e4m3fn)
+            w[r0:r0 + qf.shape[0]] *= qs      # the per-(query, head) scale is folded into the gate
+        del qf, qs
+    else:
+        q = torch.randn((nq, H, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
     pos = torch.from_numpy(rows.astype(np.int64)).to(dev).to(torch.int32)  # bit pattern == uint32 (values < 2^31)
     out_idx = torch.empty((nq, k), device=dev, dtype=torch.int32)
     out_count = torch.empty((nq,), device=dev, dtype=torch.int32)
@@ -194,9 +215,9 @@ def run_b200(a, rank, world, local_rank):
     gathered = torch.empty((world * nq, k), device=dev, dtype=torch.int32) if dist else None
     torch.cuda.synchronize()
 
-    cfg = capi.make_config(B, m, k, H, d, capi.DTYPE_BF16)
+    cfg = capi.make_config(B, m, k, H, d, capi.DTYPE_FP8 if fp8 else capi.DTYPE_BF16)
     ix = capi.Indexer(cfg, local_rank)
-    ix.upload_keys(keys.data_ptr(), seq_len=L)
+    ix.upload_keys(keys.data_ptr(), seq_len=L, scales=key_scales.data_ptr() if fp8 else None)
     ix.pool_build()
     ix.synchronize()
     stream = torch.cuda.ExternalStream(capi.lib().hisa_cuda_stream(ix._ctx), device=dev)
@@ -268,7 +289,9 @@ def run_b200(a, rank, world, local_rank):
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "kernel": "score_tc_kernel<1,2,4> (stage-2 block-major refinement)",
+    if fp8:
+        peaks = dict(peaks, tflops=2.0 * peaks["tflops"], source=peaks["source"] + " x2 for e4m3 (nominal fp8 : bf16 ratio)")
+    roofline = {"bound": "tensor", "kernel": "score_tc_kernel (stage-2 block-major refinement)",
                 "achieved": achieved, "peak": peaks["tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["tflops"], "traffic": traffic, "peak_source": peaks["source"],
                 "flops_per_launch": flops_s2, "kernel_ms": k_ms}
@@ -299,7 +322,7 @@ def run_b200(a, rank, world, local_rank):
     # ---- end to end through the C ABI with HOST buffers (pinned), copies inside the timed region
     e2e = None
     if a.e2e_steps > 0:
-        hq = torch.empty((nq, H, d), dtype=torch.bfloat16, pin_memory=True)
+        hq = torch.empty((nq, H, d), dtype=q.dtype, pin_memory=True)
         hw = torch.empty((nq, H), dtype=torch.float32, pin_memory=True)
         hpos = torch.empty((nq,), dtype=torch.int32, pin_memory=True)
         hidx = torch.empty((nq, k), dtype=torch.int32, pin_memory=True)
@@ -324,7 +347,7 @@ def run_b200(a, rank, world, local_rank):
             dt = float(t.item())
         same = bool(torch.equal(hidx.to(dev), out_idx)) if a.flat_steps == 0 else None
         e2e = {"value": Q * a.e2e_steps / dt, "unit": UNIT,
-               "h2d_bytes_per_step": int(hq.numel() * 2 + hw.numel() * 4 + hpos.numel() * 4) * world,
+               "h2d_bytes_per_step": int(hq.numel() * hq.element_size() + hw.numel() * 4 + hpos.numel() * 4) * world,
                "d2h_bytes_per_step": int(hidx.numel() * 4 + hcnt.numel() * 4) * world,
                "ms_per_step": 1e3 * dt / a.e2e_steps, "matches_device_path": same}
 
@@ -338,6 +361,8 @@ def run_b200(a, rank, world, local_rank):
         pq = q[sel_t].to(torch.float32).cpu().numpy()
         pw = w[sel_t].cpu().numpy()
         pk = keys.to(torch.float32).cpu().numpy()
+        if fp8:  # the oracle is given the dequantised keys: float(k8) * scale (one f32 rounding, as on the GPU)
+            pk = (pk * key_scales.cpu().numpy()[:, None]).astype(np.float32)
         prob = pyoracle.Problem(pq, pw, pk, rows[sel].astype(np.uint32), block_size=B, block_budget=m, token_budget=k)
         threads = pyoracle.hardware_threads()
         t0 = time.perf_counter()
@@ -357,8 +382,9 @@ def run_b200(a, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": workload_name(a), "l2": "inputs larger than L2 (q is 1 GiB per step)",
+            "dtype": "bf16" if not fp8 else "e4m3 (fp32 accumulate; block scores in bf16 hi|lo)", "data": "synthetic",
+            "config": {"workload": workload_name(a),
+                       "l2": f"inputs larger than L2 (q is {q.numel() * q.element_size() / 2**30:.1f} GiB per step)",
                        "sharding": f"query tiles of {TILE_ROWS} rows round-robin over ranks; keys NCCL-broadcast; "
                                    "indices all-gathered inside the step" if world > 1 else "single GPU"},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,

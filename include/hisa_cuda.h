@@ -60,7 +60,14 @@ typedef enum hisa_status {
 
 typedef enum hisa_dtype {
   HISA_DTYPE_F32 = 0,  /* float32 storage; scored with exact 3-way bf16 splits (fp32-grade products) */
-  HISA_DTYPE_BF16 = 1  /* bfloat16 storage, the production format */
+  HISA_DTYPE_BF16 = 1, /* bfloat16 storage, the production format */
+  /* e4m3 bytes for queries and keys (DeepSeek-V3.2 indexer format), num_heads = 64 and dim = 128 only.
+   * A key is float(k8[s, :]) * key_scale[s] (hisa_cuda_upload_keys_scaled / _pool_append_scaled; scale > 0).
+   * The per-(query, head) scale of q is folded into `gates` by the caller: gate[t, j] = w[t, j] * q_scale[t, j],
+   * which is exact because a positive scale commutes with the ReLU of Eq.1 (hisa/dsa.hpp:13-20).
+   * Token scores are computed by the e4m3 tensor-core path (tcgen05 kind::f8f6f4, fp32 accumulate); block scores
+   * multiply a bf16 copy of q (exact) with the bf16 hi|lo split of the pooled means. */
+  HISA_DTYPE_FP8_E4M3 = 2
 } hisa_dtype;
 
 typedef enum hisa_tie_break { HISA_TIE_SMALLEST_INDEX = 0, HISA_TIE_LARGEST_INDEX = 1 } hisa_tie_break;
@@ -118,11 +125,17 @@ int hisa_cuda_memcpy(hisa_cuda_ctx* ctx, void* dst, const void* src, size_t byte
 /* Replaces the sequence with `seq_len` keys [seq_len, dim] of the context dtype. EmptySequence if 0.
  * check_finite != 0 additionally scans for NaN/Inf (IndexerInputs ingestion rule, inputs.hpp:15-16). */
 int hisa_cuda_upload_keys(hisa_cuda_ctx* ctx, const void* keys, uint64_t seq_len, int check_finite);
+/* fp8 storage: same as hisa_cuda_upload_keys with per-key dequantisation scales [seq_len] (host or device; NULL = 1). */
+int hisa_cuda_upload_keys_scaled(hisa_cuda_ctx* ctx, const void* keys, const float* key_scales, uint64_t seq_len,
+                                 int check_finite);
 /* (Re)builds all block summaries of the current sequence: build_block_summaries. */
 int hisa_cuda_pool_build(hisa_cuda_ctx* ctx);
 /* Appends n keys [n, key_dim] at positions seq_len.. and updates only the touched tail blocks
  * (BlockSummaryCache::append, n times, in position order). DimensionMismatch if key_dim != dim. */
 int hisa_cuda_pool_append(hisa_cuda_ctx* ctx, const void* keys, uint64_t n, uint32_t key_dim);
+/* fp8 storage: same as hisa_cuda_pool_append with per-key dequantisation scales [n] (NULL = 1). */
+int hisa_cuda_pool_append_scaled(hisa_cuda_ctx* ctx, const void* keys, const float* key_scales, uint64_t n,
+                                 uint32_t key_dim);
 /* Reads summaries back: sums [num_blocks, dim] (double), counts [num_blocks], pooled [num_blocks, dim]
  * (double, = sum/count for Mean). Any output may be NULL. */
 int hisa_cuda_pool_read(hisa_cuda_ctx* ctx, double* sums, uint32_t* counts, double* pooled);

@@ -15,11 +15,12 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libhisa_b200.so")
 
-DTYPE_F32, DTYPE_BF16 = 0, 1
+DTYPE_F32, DTYPE_BF16, DTYPE_FP8 = 0, 1, 2
 SCORER_TENSOR, SCORER_SIMT = 0, 1
 
 # every symbol include/hisa_cuda.h declares
 EXPORTED_SYMBOLS = [
+    "hisa_cuda_upload_keys_scaled", "hisa_cuda_pool_append_scaled",
     "hisa_cuda_config_init", "hisa_cuda_config_validate", "hisa_cuda_abi_version", "hisa_cuda_status_name",
     "hisa_cuda_last_error", "hisa_cuda_device_count", "hisa_cuda_create", "hisa_cuda_destroy",
     "hisa_cuda_synchronize", "hisa_cuda_stream", "hisa_cuda_host_alloc", "hisa_cuda_host_free",
@@ -130,6 +131,53 @@ def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
     return (np.ascontiguousarray(b, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
 
 
+_E4M3_TABLE = None
+
+
+def e4m3_bits_to_f32(b: np.ndarray) -> np.ndarray:
+    """e4m3 (fn: no infinities, S.1111.111 = NaN) bytes -> float32, exactly."""
+    global _E4M3_TABLE
+    if _E4M3_TABLE is None:
+        t = np.zeros(256, np.float32)
+        for v in range(256):
+            s, e, m = v >> 7, (v >> 3) & 15, v & 7
+            if e == 15 and m == 7:
+                x = np.nan
+            elif e == 0:
+                x = m * 2.0 ** -9
+            else:
+                x = (1 + m / 8.0) * 2.0 ** (e - 7)
+            t[v] = -x if s else x
+        _E4M3_TABLE = t
+    return _E4M3_TABLE[np.ascontiguousarray(b, dtype=np.uint8)]
+
+
+def f32_to_e4m3_bits(a: np.ndarray) -> np.ndarray:
+    """float32 -> e4m3 bytes, round-to-nearest-even, saturating at +-448. Host-side data plumbing."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    mag = np.minimum(np.abs(a).astype(np.float64), 448.0)
+    e = np.floor(np.log2(np.maximum(mag, 2.0 ** -20)))
+    e = np.clip(e, -6, 8)                     # exponent of the binade (subnormals share 2^-6)
+    step = 2.0 ** (e - 3)                     # spacing of representable values in that binade
+    q = np.rint(mag / step) * step            # np.rint rounds half to even; a carry lands on the next binade exactly
+    q = np.minimum(q, 448.0)
+    ee = np.floor(np.log2(np.maximum(q, 2.0 ** -20)))
+    sub = q < 2.0 ** -6
+    exp_field = np.where(sub, 0, ee + 7).astype(np.int64)
+    man_field = np.where(sub, np.rint(q * 2.0 ** 9), np.rint((q / 2.0 ** ee - 1.0) * 8)).astype(np.int64)
+    bits = (exp_field << 3) | man_field
+    bits = np.where(q == 0, 0, bits)
+    return (bits | (np.signbit(a).astype(np.int64) << 7)).astype(np.uint8)
+
+
+def quantize_e4m3(a: np.ndarray, axis=-1):
+    """Per-row symmetric quantisation: returns (e4m3 bytes, float32 scales) with a ~= float(bytes) * scale."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    amax = np.abs(a).max(axis=axis, keepdims=True)
+    scale = np.where(amax > 0, amax / np.float32(448.0), np.float32(1.0)).astype(np.float32)
+    return f32_to_e4m3_bits(a / scale), np.squeeze(scale, axis=axis)
+
+
 def _ptr(a):
     if a is None:
         return None
@@ -173,6 +221,10 @@ class Indexer:
             return a
         if self.cfg.dtype == DTYPE_BF16:
             return np.ascontiguousarray(a if a.dtype == np.uint16 else f32_to_bf16_bits(a))
+        if self.cfg.dtype == DTYPE_FP8:
+            if a.dtype != np.uint8:
+                raise TypeError("fp8 storage takes e4m3 bytes (uint8); quantise with capi.quantize_e4m3")
+            return np.ascontiguousarray(a)
         return np.ascontiguousarray(a, dtype=np.float32)
 
     def synchronize(self): _check(lib().hisa_cuda_synchronize(self._ctx), self._ctx)
@@ -207,19 +259,31 @@ class Indexer:
         _check(lib().hisa_cuda_memcpy(self._ctx, _ptr(dst), _ptr(src), C.c_size_t(nbytes)), self._ctx)
 
     # -- keys / summaries
-    def upload_keys(self, keys, seq_len=None, check_finite=False):
+    def upload_keys(self, keys, seq_len=None, check_finite=False, scales=None):
         keys = self._elems(keys)
         L = keys.shape[0] if seq_len is None else seq_len
+        if scales is not None:
+            if isinstance(scales, np.ndarray):
+                scales = np.ascontiguousarray(scales, dtype=np.float32)
+            _check(lib().hisa_cuda_upload_keys_scaled(self._ctx, _ptr(keys), _ptr(scales), C.c_uint64(L),
+                                                      C.c_int(int(check_finite))), self._ctx)
+            return
         _check(lib().hisa_cuda_upload_keys(self._ctx, _ptr(keys), C.c_uint64(L), C.c_int(int(check_finite))), self._ctx)
 
     def pool_build(self): _check(lib().hisa_cuda_pool_build(self._ctx), self._ctx)
 
-    def pool_append(self, keys, n=None, key_dim=None):
+    def pool_append(self, keys, n=None, key_dim=None, scales=None):
         keys = self._elems(keys)
         if isinstance(keys, np.ndarray):
             keys2 = keys.reshape(-1, keys.shape[-1])
             n = keys2.shape[0] if n is None else n
             key_dim = keys2.shape[1] if key_dim is None else key_dim
+        if scales is not None:
+            if isinstance(scales, np.ndarray):
+                scales = np.ascontiguousarray(scales, dtype=np.float32)
+            _check(lib().hisa_cuda_pool_append_scaled(self._ctx, _ptr(keys), _ptr(scales), C.c_uint64(n),
+                                                      C.c_uint32(key_dim)), self._ctx)
+            return
         _check(lib().hisa_cuda_pool_append(self._ctx, _ptr(keys), C.c_uint64(n), C.c_uint32(key_dim)), self._ctx)
 
     def seq_len(self):

@@ -50,11 +50,12 @@ struct hisa_cuda_ctx {
   uint32_t terms_tok[kMaxSeg] = {1, 0, 0};
   uint32_t terms_blk[kMaxSeg] = {3, 0, 0};
   bool q_zero_copy = false;  // caller's q already is the operand (bf16, H=64, d=128)
+  bool fp8 = false;          // e4m3 storage: byte operands + per-key scales; stage 1 uses a bf16 copy of q
 
   // sequence state
   uint64_t seq_len = 0, key_cap = 0;
   uint64_t pooled_tokens = 0;  // tokens folded into the summaries so far
-  DevBuf key_op, key_raw, sums, counts, pooled_op;
+  DevBuf key_op, key_raw, key_scale, sums, counts, pooled_op;
 
   // per-call workspace
   DevBuf q_raw, q_op, gates_raw, gates_pad, pos, J, sel, nsel, work, pairs, scalars, cand, flat, out_idx, out_count,
@@ -145,7 +146,11 @@ bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-uint32_t elem_bytes(const hisa_cuda_ctx* ctx) { return ctx->cfg.dtype == HISA_DTYPE_BF16 ? 2u : 4u; }
+uint32_t elem_bytes(const hisa_cuda_ctx* ctx) {
+  return ctx->cfg.dtype == HISA_DTYPE_BF16 ? 2u : ctx->cfg.dtype == HISA_DTYPE_FP8_E4M3 ? 1u : 4u;
+}
+// element type code of the operand-preparation kernels: 0 f32, 1 bf16, 2 e4m3
+uint32_t src_type(const hisa_cuda_ctx* ctx) { return ctx->cfg.dtype == HISA_DTYPE_BF16 ? 1u : ctx->cfg.dtype == HISA_DTYPE_FP8_E4M3 ? 2u : 0u; }
 uint32_t round_up(uint32_t v, uint32_t m) { return (v + m - 1) / m * m; }
 uint64_t round_up64(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 
@@ -189,12 +194,16 @@ int check_launch(hisa_cuda_ctx* ctx, const char* what) {
   return HISA_OK;
 }
 
-int make_map(hisa_cuda_ctx* ctx, CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+// 2-D map over a row-major operand whose rows are `cols` elements; the box is one 128-byte swizzle row wide
+// (64 bf16 or 128 e4m3 elements) and `box_rows` rows tall
+int make_map(hisa_cuda_ctx* ctx, CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+             bool bytes = false) {
   cuuint64_t gdim[2] = {cols, rows ? rows : 1};
-  cuuint64_t gstride[1] = {cols * sizeof(__nv_bfloat16)};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint64_t gstride[1] = {cols * (bytes ? 1 : sizeof(__nv_bfloat16))};
+  cuuint32_t box[2] = {bytes ? 128u : 64u, box_rows};
   cuuint32_t estride[2] = {1, 1};
-  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box,
+  CUresult r = ctx->encode(map, bytes ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                           const_cast<void*>(base), gdim, gstride, box,
                            estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
@@ -212,6 +221,7 @@ uint64_t num_blocks_of(const hisa_cuda_ctx* ctx) {
 // ------------------------------------------------------------------------------------------------
 struct Prepared {
   const __nv_bfloat16* q_op = nullptr;  // [Q*64, nseg_q*128]
+  const uint8_t* q8 = nullptr;          // fp8 storage: the caller's e4m3 bytes [Q*64, 128] (stage 2 / flat operand)
   const float* gates = nullptr;         // [Q, 64]
   const uint32_t* pos = nullptr;        // [Q]
   uint64_t Q = 0;
@@ -241,7 +251,7 @@ int prepare_inputs(hisa_cuda_ctx* ctx, const void* queries, const float* gates, 
   if (Q > 0x7FFFFFFFull / kHeads) return fail(ctx, HISA_ERR_UNSUPPORTED, "too many query rows in one call");
   StageTimer timer(ctx, kStPrepare);
   const uint32_t H = ctx->cfg.num_heads, d = ctx->cfg.dim, eb = elem_bytes(ctx);
-  const bool bf16 = ctx->cfg.dtype == HISA_DTYPE_BF16;
+  const uint32_t st = src_type(ctx);
 
   // positions
   const uint32_t* pos_dev = positions;
@@ -270,7 +280,7 @@ int prepare_inputs(hisa_cuda_ctx* ctx, const void* queries, const float* gates, 
     HISA_TRY(ensure(ctx, ctx->flag, 16));
     CU_TRY(ctx, cudaMemsetAsync(ctx->flag.p, 0, 16, ctx->stream));
     uint32_t* f = ctx->flag.as<uint32_t>();
-    count_launches(ctx, launch_check_finite(q_dev, bf16, q_elems, f, ctx->stream));
+    count_launches(ctx, launch_check_finite(q_dev, st, q_elems, f, ctx->stream));
     count_launches(ctx, launch_check_finite(g_dev, 0, size_t(Q) * H, f + 1, ctx->stream));
     count_launches(ctx, launch_check_positions(pos_dev, Q, uint32_t(ctx->seq_len), f + 2, ctx->stream));
     uint32_t flags[3];
@@ -286,10 +296,11 @@ int prepare_inputs(hisa_cuda_ctx* ctx, const void* queries, const float* gates, 
     out->q_op = static_cast<const __nv_bfloat16*>(q_dev);
   } else {
     HISA_TRY(ensure(ctx, ctx->q_op, size_t(Q) * kHeads * ctx->nseg_q * kDim * sizeof(__nv_bfloat16)));
-    count_launches(ctx, launch_convert_rows(q_dev, bf16, Q, H, d, ctx->nseg_q, ctx->q_op.as<__nv_bfloat16>(), kHeads,
+    count_launches(ctx, launch_convert_rows(q_dev, st, Q, H, d, ctx->nseg_q, ctx->q_op.as<__nv_bfloat16>(), kHeads,
                                             ctx->stream));
     out->q_op = ctx->q_op.as<__nv_bfloat16>();
   }
+  if (ctx->fp8) out->q8 = static_cast<const uint8_t*>(q_dev);  // H = 64, d = 128 is required for fp8: zero-copy
   // gates are always re-laid out (padded to 64 heads, permuted to the epilogue's lane order): 256 B per query
   HISA_TRY(ensure(ctx, ctx->gates_pad, size_t(Q) * kHeads * sizeof(float)));
   count_launches(ctx, launch_permute_gates(g_dev, Q, H, ctx->gates_pad.as<float>(), ctx->stream));
@@ -316,6 +327,10 @@ struct ScoreJob {
   bool list_mode;
   const uint2* pairs;
   uint32_t max_items;
+  // fp8 storage (stage 2 / flat only): byte operands and the per-key scale
+  const uint8_t* a8 = nullptr;
+  const uint8_t* q8 = nullptr;
+  const float* a_scale = nullptr;
 };
 
 int run_scorer(hisa_cuda_ctx* ctx, const ScoreJob& j) {
@@ -336,6 +351,8 @@ int run_scorer(hisa_cuda_ctx* ctx, const ScoreJob& j) {
   a.nseg_b = ctx->nseg_q;
   for (int i = 0; i < kMaxSeg; ++i) a.terms[i] = j.terms[i];
   a.a_rows = uint32_t(j.a_rows);
+  a.fp8 = j.a8 ? 1u : 0u;
+  a.a_scale = j.a_scale;
   a.debug_flags = env_u32("HISA_TC_DEBUG", 0);
   a.stats = nullptr;
   if (ctx->profiling) {
@@ -349,13 +366,35 @@ int run_scorer(hisa_cuda_ctx* ctx, const ScoreJob& j) {
     count_launches(ctx, launch_score_simt(a, j.a_op, j.q_op, j.max_items, ctx->stream));
   } else {
     CUtensorMap map_a, map_b;
-    HISA_TRY(make_map(ctx, &map_a, j.a_op, j.a_rows, uint64_t(j.nseg_a) * kDim, kTileRows));
-    HISA_TRY(make_map(ctx, &map_b, j.q_op, j.nq * kHeads, uint64_t(ctx->nseg_q) * kDim, kHeads));
+    if (j.a8) {
+      a.nseg_a = a.nseg_b = 1;
+      HISA_TRY(make_map(ctx, &map_a, j.a8, j.a_rows, kDim, kTileRows, true));
+      HISA_TRY(make_map(ctx, &map_b, j.q8, j.nq * kHeads, kDim, kHeads, true));
+    } else {
+      HISA_TRY(make_map(ctx, &map_a, j.a_op, j.a_rows, uint64_t(j.nseg_a) * kDim, kTileRows));
+      HISA_TRY(make_map(ctx, &map_b, j.q_op, j.nq * kHeads, uint64_t(ctx->nseg_q) * kDim, kHeads));
+    }
     const int n = launch_score_tc(a, map_a, map_b, ctx->num_sms, ctx->stream);
     if (n < 0) return fail(ctx, HISA_ERR_UNSUPPORTED, "no tensor-core scorer variant for this operand segment structure");
     count_launches(ctx, n);
   }
   return check_launch(ctx, "scorer");
+}
+
+// operands of a token-scoring job (stage 2, flat, score_tokens) for query rows [q0, ...)
+void set_token_operands(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, ScoreJob& j) {
+  j.a_rows = ctx->seq_len;
+  j.terms = ctx->terms_tok;
+  if (ctx->fp8) {
+    j.a8 = ctx->key_op.as<uint8_t>();
+    j.q8 = p.q8 + q0 * kHeads * kDim;
+    j.a_scale = ctx->key_scale.as<float>();
+    j.nseg_a = 1;
+  } else {
+    j.a_op = ctx->key_op.as<__nv_bfloat16>();
+    j.nseg_a = ctx->nseg_k;
+    j.q_op = p.q_op + q0 * kHeads * ctx->nseg_q * kDim;
+  }
 }
 
 int ensure_pool(hisa_cuda_ctx* ctx) {
@@ -505,11 +544,7 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
                                                     ctx->work.as<WorkItem>(), sc, sc + 1, ctx->stream));
         ScoreJob j{};
         j.stats_slot = 1;
-        j.a_op = ctx->key_op.as<__nv_bfloat16>();
-        j.a_rows = L;
-        j.nseg_a = ctx->nseg_k;
-        j.terms = ctx->terms_tok;
-        j.q_op = p.q_op + q0 * kHeads * ctx->nseg_q * kDim;
+        set_token_operands(ctx, p, q0, j);
         j.nq = nq;
         j.gates = p.gates + q0 * kHeads;
         j.out = ctx->flat.as<float>();
@@ -570,11 +605,7 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
           StageTimer timer(ctx, kStScoreTokens);
           ScoreJob j{};
           j.stats_slot = 1;
-          j.a_op = ctx->key_op.as<__nv_bfloat16>();
-          j.a_rows = L;
-          j.nseg_a = ctx->nseg_k;
-          j.terms = ctx->terms_tok;
-          j.q_op = p.q_op + q0 * kHeads * ctx->nseg_q * kDim;
+          set_token_operands(ctx, p, q0, j);
           j.nq = nq;
           j.gates = p.gates + q0 * kHeads;
           j.out = ctx->cand.as<float>();
@@ -822,8 +853,12 @@ int hisa_cuda_create(int device, const hisa_cuda_config* cfg, hisa_cuda_ctx** ou
     return fail(nullptr, HISA_ERR_UNSUPPORTED, "num_heads %u > %d is not covered by the sm_100a kernels", cfg->num_heads, kHeads);
   if (cfg->dim > uint32_t(kDim))
     return fail(nullptr, HISA_ERR_UNSUPPORTED, "dim %u > %d is not covered by the sm_100a kernels", cfg->dim, kDim);
-  if (cfg->dtype != HISA_DTYPE_F32 && cfg->dtype != HISA_DTYPE_BF16)
+  if (cfg->dtype != HISA_DTYPE_F32 && cfg->dtype != HISA_DTYPE_BF16 && cfg->dtype != HISA_DTYPE_FP8_E4M3)
     return fail(nullptr, HISA_ERR_UNSUPPORTED, "unknown dtype %u", cfg->dtype);
+  if (cfg->dtype == HISA_DTYPE_FP8_E4M3 && (cfg->num_heads != uint32_t(kHeads) || cfg->dim != uint32_t(kDim)))
+    return fail(nullptr, HISA_ERR_UNSUPPORTED, "fp8 storage is built for num_heads = %d, dim = %d only", kHeads, kDim);
+  if (cfg->dtype == HISA_DTYPE_FP8_E4M3 && cfg->scorer == HISA_SCORER_SIMT)
+    return fail(nullptr, HISA_ERR_UNSUPPORTED, "the SIMT cross-check scorer does not read fp8 operands");
   if (cfg->tie_break > 1 || cfg->pool_mode > 1 || cfg->scorer > 1)
     return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "config enum field out of range");
   if (uint64_t(cfg->block_budget) + 2 > 0xFFFFFFull || uint64_t(cfg->block_budget + 2) * cfg->block_size > 0x7FFFFFFFull)
@@ -858,7 +893,10 @@ int hisa_cuda_create(int device, const hisa_cuda_config* cfg, hisa_cuda_ctx** ou
   ctx->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
 
   const bool bf16 = cfg->dtype == HISA_DTYPE_BF16;
-  if (bf16) {
+  ctx->fp8 = cfg->dtype == HISA_DTYPE_FP8_E4M3;
+  if (bf16 || ctx->fp8) {
+    // fp8: stage 1 multiplies a bf16 copy of q (e4m3 values are exact in bf16) with the bf16 hi|lo pooled keys;
+    // stage 2 and the flat scorer read the e4m3 bytes of q and k directly
     ctx->nseg_k = ctx->nseg_q = 1;
     ctx->nseg_p = std::min<uint32_t>(std::max<uint32_t>(env_u32("HISA_POOL_SEGS", 2), 1), kMaxSeg);
     ctx->terms_tok[0] = 1; ctx->terms_tok[1] = ctx->terms_tok[2] = 0;
@@ -882,7 +920,7 @@ int hisa_cuda_destroy(hisa_cuda_ctx* ctx) {
   if (!ctx) return HISA_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (DevBuf* b : {&ctx->key_op, &ctx->key_raw, &ctx->sums, &ctx->counts, &ctx->pooled_op, &ctx->q_raw, &ctx->q_op,
+  for (DevBuf* b : {&ctx->key_op, &ctx->key_raw, &ctx->key_scale, &ctx->sums, &ctx->counts, &ctx->pooled_op, &ctx->q_raw, &ctx->q_op,
                     &ctx->gates_raw, &ctx->gates_pad, &ctx->pos, &ctx->J, &ctx->sel, &ctx->nsel, &ctx->work, &ctx->pairs,
                     &ctx->scalars, &ctx->cand, &ctx->flat, &ctx->out_idx, &ctx->out_count, &ctx->out_cand,
                     &ctx->generic_scores, &ctx->generic_n, &ctx->export_a, &ctx->export_b, &ctx->flag, &ctx->stats})
@@ -950,10 +988,14 @@ static int grow_keys(hisa_cuda_ctx* ctx, uint64_t need_tokens) {
   if (need_tokens <= ctx->key_cap) return HISA_OK;
   uint64_t cap = std::max<uint64_t>(need_tokens, ctx->key_cap + ctx->key_cap / 2);
   cap = round_up64(cap, 1024);
-  const size_t row_bytes = size_t(ctx->nseg_k) * kDim * sizeof(__nv_bfloat16);
+  const size_t row_bytes = ctx->fp8 ? size_t(kDim) : size_t(ctx->nseg_k) * kDim * sizeof(__nv_bfloat16);
   const uint64_t mcap = (cap + ctx->cfg.block_size - 1) / ctx->cfg.block_size + 1;
-  DevBuf nk, ns, nc, np;
+  DevBuf nk, ns, nc, np, nsc;
   CU_TRY(ctx, cudaMalloc(&nk.p, cap * row_bytes));
+  if (ctx->fp8) {
+    CU_TRY(ctx, cudaMalloc(&nsc.p, cap * sizeof(float)));
+    nsc.cap = cap * sizeof(float);
+  }
   CU_TRY(ctx, cudaMalloc(&ns.p, mcap * kDim * sizeof(double)));
   CU_TRY(ctx, cudaMalloc(&nc.p, mcap * sizeof(uint32_t)));
   CU_TRY(ctx, cudaMalloc(&np.p, mcap * ctx->nseg_p * kDim * sizeof(__nv_bfloat16)));
@@ -963,25 +1005,29 @@ static int grow_keys(hisa_cuda_ctx* ctx, uint64_t need_tokens) {
   if (ctx->seq_len) {
     const uint64_t M = num_blocks_of(ctx);
     CU_TRY(ctx, cudaMemcpyAsync(nk.p, ctx->key_op.p, ctx->seq_len * row_bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (ctx->fp8)
+      CU_TRY(ctx, cudaMemcpyAsync(nsc.p, ctx->key_scale.p, ctx->seq_len * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
     CU_TRY(ctx, cudaMemcpyAsync(ns.p, ctx->sums.p, M * kDim * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
     CU_TRY(ctx, cudaMemcpyAsync(nc.p, ctx->counts.p, M * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
     CU_TRY(ctx, cudaMemcpyAsync(np.p, ctx->pooled_op.p, M * ctx->nseg_p * kDim * sizeof(__nv_bfloat16),
                                 cudaMemcpyDeviceToDevice, ctx->stream));
   }
   CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  release(ctx->key_op); release(ctx->sums); release(ctx->counts); release(ctx->pooled_op);
-  ctx->key_op = nk; ctx->sums = ns; ctx->counts = nc; ctx->pooled_op = np;
+  release(ctx->key_op); release(ctx->sums); release(ctx->counts); release(ctx->pooled_op); release(ctx->key_scale);
+  ctx->key_op = nk; ctx->sums = ns; ctx->counts = nc; ctx->pooled_op = np; ctx->key_scale = nsc;
   ctx->key_cap = cap;
   return HISA_OK;
 }
 
 // converts n keys (host or device, ctx dtype, [n, dim]) into operand rows [first, first+n)
-static int ingest_keys(hisa_cuda_ctx* ctx, const void* keys, uint64_t first, uint64_t n, int check_finite) {
+// fp8: `scales` (host or device, may be null = 1) are the per-key dequantisation scales
+static int ingest_keys(hisa_cuda_ctx* ctx, const void* keys, const float* scales, uint64_t first, uint64_t n,
+                       int check_finite) {
   const uint32_t d = ctx->cfg.dim, eb = elem_bytes(ctx);
-  const bool bf16 = ctx->cfg.dtype == HISA_DTYPE_BF16;
+  const uint32_t st = src_type(ctx);
   const void* src = keys;
-  const bool direct = bf16 && d == uint32_t(kDim);
-  __nv_bfloat16* dst = ctx->key_op.as<__nv_bfloat16>() + first * ctx->nseg_k * kDim;
+  const bool direct = (st == 1 || st == 2) && d == uint32_t(kDim);
+  void* dst = ctx->key_op.as<uint8_t>() + first * (ctx->fp8 ? size_t(kDim) : size_t(ctx->nseg_k) * kDim * sizeof(__nv_bfloat16));
   if (direct) {
     HISA_TRY(copy_in(ctx, dst, keys, n * d * eb));
     src = dst;
@@ -990,60 +1036,95 @@ static int ingest_keys(hisa_cuda_ctx* ctx, const void* keys, uint64_t first, uin
     HISA_TRY(copy_in(ctx, ctx->key_raw.p, keys, n * d * eb));
     src = ctx->key_raw.p;
   }
+  if (ctx->fp8) {
+    float* sdst = ctx->key_scale.as<float>() + first;
+    if (scales) HISA_TRY(copy_in(ctx, sdst, scales, n * sizeof(float)));
+    else count_launches(ctx, launch_fill_f32(sdst, n, 1.0f, ctx->stream));
+  }
   if (check_finite) {
     HISA_TRY(ensure(ctx, ctx->flag, 16));
     CU_TRY(ctx, cudaMemsetAsync(ctx->flag.p, 0, 16, ctx->stream));
-    count_launches(ctx, launch_check_finite(src, bf16, n * d, ctx->flag.as<uint32_t>(), ctx->stream));
+    count_launches(ctx, launch_check_finite(src, st, n * d, ctx->flag.as<uint32_t>(), ctx->stream));
+    if (ctx->fp8) count_launches(ctx, launch_check_finite(ctx->key_scale.as<float>() + first, 0, n, ctx->flag.as<uint32_t>(), ctx->stream));
     uint32_t bad = 0;
     HISA_TRY(read_flag(ctx, &bad));
     if (bad) return fail(ctx, HISA_ERR_NON_FINITE, "inputs: non-finite value in keys");
   }
   if (!direct)
-    count_launches(ctx, launch_convert_rows(src, bf16, n, 1, d, ctx->nseg_k, dst, 1, ctx->stream));
+    count_launches(ctx, launch_convert_rows(src, st, n, 1, d, ctx->nseg_k, static_cast<__nv_bfloat16*>(dst), 1, ctx->stream));
   return check_launch(ctx, "key ingestion");
 }
 
-int hisa_cuda_upload_keys(hisa_cuda_ctx* ctx, const void* keys, uint64_t seq_len, int check_finite) {
+static int pool_update(hisa_cuda_ctx* ctx, uint64_t first, uint64_t n) {
+  if (ctx->fp8)
+    count_launches(ctx, launch_pool_update_fp8(ctx->key_op.as<uint8_t>(), ctx->key_scale.as<float>(), first, n,
+                                               ctx->cfg.block_size, ctx->cfg.pool_mode, ctx->sums.as<double>(),
+                                               ctx->counts.as<uint32_t>(), ctx->pooled_op.as<__nv_bfloat16>(), ctx->nseg_p,
+                                               ctx->stream));
+  else
+    count_launches(ctx, launch_pool_update(ctx->key_op.as<__nv_bfloat16>(), ctx->nseg_k, first, n, ctx->cfg.block_size,
+                                           ctx->cfg.dim, ctx->cfg.pool_mode, ctx->sums.as<double>(), ctx->counts.as<uint32_t>(),
+                                           ctx->pooled_op.as<__nv_bfloat16>(), ctx->nseg_p, ctx->stream));
+  return HISA_OK;
+}
+
+static int upload_keys_impl(hisa_cuda_ctx* ctx, const void* keys, const float* scales, uint64_t seq_len, int check_finite) {
   if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
   CU_TRY(ctx, cudaSetDevice(ctx->device));
   if (seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "upload_keys: key matrix has no rows");
   if (!keys) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "null keys");
+  if (scales && !ctx->fp8) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "key scales are only meaningful for fp8 storage");
   if (seq_len > 0x7FFFFF00ull) return fail(ctx, HISA_ERR_UNSUPPORTED, "sequence too long");
   ctx->seq_len = 0;
   ctx->pooled_tokens = 0;
   HISA_TRY(grow_keys(ctx, seq_len));
-  HISA_TRY(ingest_keys(ctx, keys, 0, seq_len, check_finite));
+  HISA_TRY(ingest_keys(ctx, keys, scales, 0, seq_len, check_finite));
   ctx->seq_len = seq_len;
   return HISA_OK;
 }
 
-int hisa_cuda_pool_build(hisa_cuda_ctx* ctx) {
-  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
-  CU_TRY(ctx, cudaSetDevice(ctx->device));
-  if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "build_block_summaries: key matrix has no rows");
-  count_launches(ctx, launch_pool_update(ctx->key_op.as<__nv_bfloat16>(), ctx->nseg_k, 0, ctx->seq_len, ctx->cfg.block_size,
-                                         ctx->cfg.dim, ctx->cfg.pool_mode, ctx->sums.as<double>(), ctx->counts.as<uint32_t>(),
-                                         ctx->pooled_op.as<__nv_bfloat16>(), ctx->nseg_p, ctx->stream));
-  ctx->pooled_tokens = ctx->seq_len;
-  return check_launch(ctx, "pool build");
-}
-
-int hisa_cuda_pool_append(hisa_cuda_ctx* ctx, const void* keys, uint64_t n, uint32_t key_dim) {
+static int pool_append_impl(hisa_cuda_ctx* ctx, const void* keys, const float* scales, uint64_t n, uint32_t key_dim) {
   if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
   CU_TRY(ctx, cudaSetDevice(ctx->device));
   if (key_dim != ctx->cfg.dim)
     return fail(ctx, HISA_ERR_DIMENSION_MISMATCH, "append: key has %u components, cache dimension is %u", key_dim, ctx->cfg.dim);
   if (n == 0) return HISA_OK;
   if (!keys) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "null keys");
+  if (scales && !ctx->fp8) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "key scales are only meaningful for fp8 storage");
   if (ctx->pooled_tokens != ctx->seq_len) HISA_TRY(hisa_cuda_pool_build(ctx));
   HISA_TRY(grow_keys(ctx, ctx->seq_len + n));
-  HISA_TRY(ingest_keys(ctx, keys, ctx->seq_len, n, 0));
-  count_launches(ctx, launch_pool_update(ctx->key_op.as<__nv_bfloat16>(), ctx->nseg_k, ctx->seq_len, n, ctx->cfg.block_size,
-                                         ctx->cfg.dim, ctx->cfg.pool_mode, ctx->sums.as<double>(), ctx->counts.as<uint32_t>(),
-                                         ctx->pooled_op.as<__nv_bfloat16>(), ctx->nseg_p, ctx->stream));
+  HISA_TRY(ingest_keys(ctx, keys, scales, ctx->seq_len, n, 0));
+  HISA_TRY(pool_update(ctx, ctx->seq_len, n));
   ctx->seq_len += n;
   ctx->pooled_tokens = ctx->seq_len;
   return check_launch(ctx, "pool append");
+}
+
+int hisa_cuda_upload_keys(hisa_cuda_ctx* ctx, const void* keys, uint64_t seq_len, int check_finite) {
+  return upload_keys_impl(ctx, keys, nullptr, seq_len, check_finite);
+}
+
+int hisa_cuda_upload_keys_scaled(hisa_cuda_ctx* ctx, const void* keys, const float* key_scales, uint64_t seq_len,
+                                 int check_finite) {
+  return upload_keys_impl(ctx, keys, key_scales, seq_len, check_finite);
+}
+
+int hisa_cuda_pool_build(hisa_cuda_ctx* ctx) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "build_block_summaries: key matrix has no rows");
+  HISA_TRY(pool_update(ctx, 0, ctx->seq_len));
+  ctx->pooled_tokens = ctx->seq_len;
+  return check_launch(ctx, "pool build");
+}
+
+int hisa_cuda_pool_append(hisa_cuda_ctx* ctx, const void* keys, uint64_t n, uint32_t key_dim) {
+  return pool_append_impl(ctx, keys, nullptr, n, key_dim);
+}
+
+int hisa_cuda_pool_append_scaled(hisa_cuda_ctx* ctx, const void* keys, const float* key_scales, uint64_t n,
+                                 uint32_t key_dim) {
+  return pool_append_impl(ctx, keys, key_scales, n, key_dim);
 }
 
 int hisa_cuda_pool_read(hisa_cuda_ctx* ctx, double* sums, uint32_t* counts, double* pooled) {
@@ -1217,11 +1298,7 @@ int hisa_cuda_score_tokens(hisa_cuda_ctx* ctx, const void* queries, const float*
   count_launches(ctx, launch_build_dense_work(p.pos, uint32_t(Q), ctx->chunk_dense, L, 1, ntiles, ctx->work.as<WorkItem>(),
                                               sc, sc + 1, ctx->stream));
   ScoreJob j{};
-  j.a_op = ctx->key_op.as<__nv_bfloat16>();
-  j.a_rows = L;
-  j.nseg_a = ctx->nseg_k;
-  j.terms = ctx->terms_tok;
-  j.q_op = p.q_op;
+  set_token_operands(ctx, p, 0, j);
   j.nq = Q;
   j.gates = p.gates;
   j.out = out_dev ? out_scores : ctx->flat.as<float>();

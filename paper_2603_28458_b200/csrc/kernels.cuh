@@ -51,6 +51,8 @@ struct ScoreArgs {
   uint32_t nseg_a, nseg_b;     // operand segments of the tile (A) and query (B) operands
   uint32_t terms[kMaxSeg];     // terms[ib] = bit mask of A segments multiplied with B segment ib
   uint32_t a_rows;             // rows that exist in the A operand (rows beyond read as zero)
+  uint32_t fp8;                // operands are e4m3 bytes [rows, 128] (kind::f8f6f4); nseg_a = nseg_b = 1
+  const float* a_scale;        // fp8: per-row dequantisation scale of the A operand (may be null = 1)
   uint32_t debug_flags;        // timing experiments only (HISA_TC_DEBUG): 1 skip epilogue math, 2 skip query TMA
   unsigned long long* stats;   // optional [kScoreStats] role-level stall cycles, summed over CTAs (may be null)
 };
@@ -135,16 +137,21 @@ int launch_expand_blocks(const int32_t* sel, const uint32_t* nsel, uint32_t sel_
                          uint32_t out_width, uint32_t* out_count, cudaStream_t stream);
 
 // operand preparation
-int launch_convert_rows(const void* src, uint32_t src_is_bf16, uint64_t rows, uint32_t src_heads_or_1,
+// src_type: 0 = f32, 1 = bf16, 2 = e4m3 bytes
+int launch_convert_rows(const void* src, uint32_t src_type, uint64_t rows, uint32_t src_heads_or_1,
                         uint32_t src_dim, uint32_t nseg, __nv_bfloat16* dst, uint32_t dst_heads_or_1,
                         cudaStream_t stream);
 int launch_permute_gates(const float* src, uint64_t rows, uint32_t heads, float* dst, cudaStream_t stream);
-int launch_check_finite(const void* src, uint32_t is_bf16, uint64_t n, uint32_t* flag, cudaStream_t stream);
+int launch_check_finite(const void* src, uint32_t src_type, uint64_t n, uint32_t* flag, cudaStream_t stream);
 int launch_check_positions(const uint32_t* pos, uint64_t n, uint32_t seq_len, uint32_t* flag, cudaStream_t stream);
 // block summaries over tokens [first, first+n): double sums, counts, pooled operand (nseg_p segments)
 int launch_pool_update(const __nv_bfloat16* key_op, uint32_t nseg_k, uint64_t first, uint64_t n, uint32_t block_size,
                        uint32_t dim, uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op,
                        uint32_t nseg_p, cudaStream_t stream);
+int launch_pool_update_fp8(const uint8_t* key8, const float* key_scale, uint64_t first, uint64_t n, uint32_t block_size,
+                           uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op, uint32_t nseg_p,
+                           cudaStream_t stream);
+int launch_fill_f32(float* dst, uint64_t n, float v, cudaStream_t stream);
 int launch_pool_export(const double* sums, const uint32_t* counts, uint32_t num_blocks, uint32_t dim,
                        uint32_t pool_max, double* out_sums, double* out_pooled, cudaStream_t stream);
 

@@ -7,9 +7,21 @@
 // bit with each other and with a CPU loop in the same order.
 #include "kernels.cuh"
 
+#include <cuda_fp8.h>
+
 namespace hisa_dev {
 
 namespace {
+
+__device__ __forceinline__ float e4m3_to_float(uint8_t b) {
+  return __half2float(__half(__nv_cvt_fp8_to_halfraw(b, __NV_E4M3)));  // exact: every e4m3 value is a half value
+}
+// element `i` of a source array of type code 0 = f32, 1 = bf16, 2 = e4m3
+__device__ __forceinline__ float load_elem(const void* src, uint32_t type, uint64_t i) {
+  if (type == 1) return __bfloat162float(static_cast<const __nv_bfloat16*>(src)[i]);
+  if (type == 2) return e4m3_to_float(static_cast<const uint8_t*>(src)[i]);
+  return static_cast<const float*>(src)[i];
+}
 
 __device__ __forceinline__ void split_bf16(float x, int nseg, __nv_bfloat16* parts) {
   // exact multi-term bf16 expansion of an fp32 value: x == parts[0] + parts[1] + parts[2] for nseg = 3
@@ -25,7 +37,7 @@ __device__ __forceinline__ void split_bf16(float x, int nseg, __nv_bfloat16* par
 
 // dst row (o*dst_heads + h) <- src row (o*src_heads + h) for h < src_heads, zero rows otherwise;
 // columns >= src_dim are zero. One thread per (dst row, 8-column group).
-__global__ void convert_rows_kernel(const void* __restrict__ src, uint32_t src_is_bf16, uint64_t outer,
+__global__ void convert_rows_kernel(const void* __restrict__ src, uint32_t src_type, uint64_t outer,
                                     uint32_t src_heads, uint32_t src_dim, uint32_t nseg,
                                     __nv_bfloat16* __restrict__ dst, uint32_t dst_heads) {
   const uint64_t gid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -44,8 +56,7 @@ __global__ void convert_rows_kernel(const void* __restrict__ src, uint32_t src_i
     for (int i = 0; i < 8; ++i) {
       const uint32_t c = cg * 8 + i;
       if (c < src_dim) {
-        v[i] = src_is_bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(src)[srow * src_dim + c])
-                           : static_cast<const float*>(src)[srow * src_dim + c];
+        v[i] = load_elem(src, src_type, srow * src_dim + c);
       }
     }
   }
@@ -74,13 +85,11 @@ __global__ void permute_gates_kernel(const float* __restrict__ src, uint64_t row
   dst[r * kHeads + gate_slot(h)] = h < heads ? src[r * heads + h] : 0.f;
 }
 
-__global__ void check_finite_kernel(const void* __restrict__ src, uint32_t is_bf16, uint64_t n,
+__global__ void check_finite_kernel(const void* __restrict__ src, uint32_t src_type, uint64_t n,
                                     uint32_t* __restrict__ flag) {
   bool bad = false;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-    const float v = is_bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(src)[i])
-                            : static_cast<const float*>(src)[i];
-    bad |= !isfinite(v);
+    bad |= !isfinite(load_elem(src, src_type, i));  // e4m3 has no infinities; S.1111.111 decodes to NaN
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
@@ -121,6 +130,39 @@ pool_update_kernel(const __nv_bfloat16* __restrict__ key_op, uint32_t nseg_k, ui
   for (uint32_t g = 0; g < nseg_p; ++g) pooled_op[b * (uint64_t(nseg_p) * kDim) + g * kDim + c] = parts[g];
 }
 
+// Same accumulation for e4m3 keys with a per-key scale: the summed value is float(k8) * scale (one f32 rounding),
+// exactly what the CPU oracle is given as the dequantised key.
+__global__ void __launch_bounds__(kDim)
+pool_update_fp8_kernel(const uint8_t* __restrict__ key8, const float* __restrict__ key_scale, uint64_t first, uint64_t n,
+                       uint32_t block_size, uint32_t pool_max, double* __restrict__ sums,
+                       uint32_t* __restrict__ counts, __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p) {
+  const uint64_t b = first / block_size + blockIdx.x;
+  const uint32_t c = threadIdx.x;
+  const uint64_t blk_lo = b * block_size;
+  const uint64_t s_lo = first > blk_lo ? first : blk_lo;
+  const uint64_t blk_hi = blk_lo + block_size;
+  const uint64_t s_hi = (first + n) < blk_hi ? (first + n) : blk_hi;
+  const bool fresh = (s_lo == blk_lo);
+  double acc = fresh ? 0.0 : sums[b * kDim + c];
+  for (uint64_t s = s_lo; s < s_hi; ++s) {
+    const double v = double(e4m3_to_float(key8[s * kDim + c]) * key_scale[s]);
+    if (pool_max) acc = (fresh && s == s_lo) ? v : (v > acc ? v : acc);
+    else acc += v;
+  }
+  sums[b * kDim + c] = acc;
+  const uint32_t cnt = uint32_t(s_hi - blk_lo);
+  if (c == 0) counts[b] = cnt;
+  const double p = pool_max ? acc : acc / double(cnt);
+  __nv_bfloat16 parts[kMaxSeg];
+  split_bf16(float(p), int(nseg_p), parts);
+  for (uint32_t g = 0; g < nseg_p; ++g) pooled_op[b * (uint64_t(nseg_p) * kDim) + g * kDim + c] = parts[g];
+}
+
+__global__ void fill_f32_kernel(float* __restrict__ dst, uint64_t n, float v) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = v;
+}
+
 __global__ void pool_export_kernel(const double* __restrict__ sums, const uint32_t* __restrict__ counts,
                                    uint32_t num_blocks, uint32_t dim, uint32_t pool_max,
                                    double* __restrict__ out_sums, double* __restrict__ out_pooled) {
@@ -137,11 +179,11 @@ inline uint32_t blocks_for(uint64_t n, uint32_t threads) { return uint32_t((n + 
 
 }  // namespace
 
-int launch_convert_rows(const void* src, uint32_t src_is_bf16, uint64_t outer, uint32_t src_heads, uint32_t src_dim,
+int launch_convert_rows(const void* src, uint32_t src_type, uint64_t outer, uint32_t src_heads, uint32_t src_dim,
                         uint32_t nseg, __nv_bfloat16* dst, uint32_t dst_heads, cudaStream_t stream) {
   const uint64_t total = outer * dst_heads * (kDim / 8);
   if (total == 0) return 0;
-  convert_rows_kernel<<<blocks_for(total, 256), 256, 0, stream>>>(src, src_is_bf16, outer, src_heads, src_dim, nseg,
+  convert_rows_kernel<<<blocks_for(total, 256), 256, 0, stream>>>(src, src_type, outer, src_heads, src_dim, nseg,
                                                                   dst, dst_heads);
   return 1;
 }
@@ -152,10 +194,10 @@ int launch_permute_gates(const float* src, uint64_t rows, uint32_t heads, float*
   return 1;
 }
 
-int launch_check_finite(const void* src, uint32_t is_bf16, uint64_t n, uint32_t* flag, cudaStream_t stream) {
+int launch_check_finite(const void* src, uint32_t src_type, uint64_t n, uint32_t* flag, cudaStream_t stream) {
   if (n == 0) return 0;
   const uint32_t grid = uint32_t(n / 256 + 1 < 148 * 16 ? n / 256 + 1 : 148 * 16);
-  check_finite_kernel<<<grid, 256, 0, stream>>>(src, is_bf16, n, flag);
+  check_finite_kernel<<<grid, 256, 0, stream>>>(src, src_type, n, flag);
   return 1;
 }
 
@@ -172,6 +214,22 @@ int launch_pool_update(const __nv_bfloat16* key_op, uint32_t nseg_k, uint64_t fi
   const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
   pool_update_kernel<<<uint32_t(b1 - b0 + 1), kDim, 0, stream>>>(key_op, nseg_k, first, n, block_size, pool_max, sums,
                                                                  counts, pooled_op, nseg_p);
+  return 1;
+}
+
+int launch_pool_update_fp8(const uint8_t* key8, const float* key_scale, uint64_t first, uint64_t n, uint32_t block_size,
+                           uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op, uint32_t nseg_p,
+                           cudaStream_t stream) {
+  if (n == 0) return 0;
+  const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
+  pool_update_fp8_kernel<<<uint32_t(b1 - b0 + 1), kDim, 0, stream>>>(key8, key_scale, first, n, block_size, pool_max, sums,
+                                                                     counts, pooled_op, nseg_p);
+  return 1;
+}
+
+int launch_fill_f32(float* dst, uint64_t n, float v, cudaStream_t stream) {
+  if (n == 0) return 0;
+  fill_f32_kernel<<<blocks_for(n, 256), 256, 0, stream>>>(dst, n, v);
   return 1;
 }
 

@@ -47,7 +47,6 @@ constexpr int kTcThreads = 11 * 32;
 constexpr int kMetaSlots = 8;
 constexpr int kUnitSlots = 4;
 constexpr uint32_t kAHalfBytes = kTileRows * 128;      // one 64-element K-half of one A segment: 16 KB
-constexpr uint32_t kASegBytes = 2 * kAHalfBytes;       // 32 KB
 constexpr uint32_t kQBoxBytes = kHeads * 128;          // one query, one K-half: 8 KB
 constexpr uint32_t kBChunkBytes = kGroupQ * kQBoxBytes;  // 32 KB
 constexpr uint32_t kGateRowBytes = kHeads * 4;         // 256 B
@@ -65,10 +64,10 @@ struct GroupMeta {
 };
 static_assert(sizeof(GroupMeta) == 48, "GroupMeta fields are read by byte offset");
 
-template <int NSEG_A, int ABUF, int NST>
+template <int NSEG_A, int ABUF, int NST, int KH>
 struct SmemLayout {
   static constexpr uint32_t a_off = 0;
-  static constexpr uint32_t b_off = a_off + ABUF * NSEG_A * kASegBytes;
+  static constexpr uint32_t b_off = a_off + ABUF * NSEG_A * KH * kAHalfBytes;
   static constexpr uint32_t w_off = b_off + NST * kBChunkBytes;
   static constexpr uint32_t meta_off = w_off + kMetaSlots * kGroupQ * kGateRowBytes;
   static constexpr uint32_t unit_off = meta_off + kMetaSlots * sizeof(GroupMeta);
@@ -121,6 +120,7 @@ __device__ __forceinline__ void load_gates(float4 (&gw)[4], uint32_t waddr) {
 // covered by the reduction of the next half-fragment.
 struct RowSum {
   float keep0, keep1, got0, got1;
+  float scale;  // per-key dequantisation scale (fp8 operands), 1 otherwise
   float* dst;
   bool ok;
   __device__ __forceinline__ void step1(const float2& a0, const float2& a1, const float2& a2, const float2& a3, bool b0) {
@@ -136,15 +136,22 @@ struct RowSum {
     got0 = __shfl_xor_sync(0xffffffffu, b1 ? k0 : k1, 2);
   }
   __device__ __forceinline__ void step3() {
-    if (ok) *dst = keep0 + got0;
+    if (ok) *dst = (keep0 + got0) * scale;
   }
 };
 
 // TERMS: bit (ib * 3 + ia) set <=> A segment ia is multiplied with B segment ib
-template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST>
+// FP8: operands are e4m3 bytes (kind::f8f6f4, K = 32 per instruction): a 128-element row is ONE 128-byte swizzle
+// row, so a segment is a single K slab (KH = 1) where bf16 needs two (KH = 2), and a group needs one 32 KB query
+// chunk instead of two; the per-key dequantisation scale multiplies the finished row sum (scale > 0 commutes with
+// the ReLU), the per-(query, head) scale is part of the gate.
+template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8>
 __global__ void __launch_bounds__(kTcThreads, 1)
 score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, ScoreArgs a) {
-  using L = SmemLayout<NSEG_A, ABUF, NST>;
+  constexpr int KH = FP8 ? 1 : 2;                     // 128-byte K slabs per operand segment
+  constexpr int KBOX = FP8 ? 128 : 64;                // elements per slab
+  constexpr uint32_t kASegBytes = KH * kAHalfBytes;   // one A segment: 16 KB (fp8) / 32 KB (bf16)
+  using L = SmemLayout<NSEG_A, ABUF, NST, KH>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // dynamic smem is only guaranteed 16-byte aligned: round up to the 1024 B the 128B swizzle needs
   // (pointer arithmetic on the __shared__ array keeps the address space known to the compiler: LDS/STS, not generic)
@@ -249,9 +256,9 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 #pragma unroll
         for (int ia = 0; ia < NSEG_A; ++ia)
 #pragma unroll
-          for (int kh = 0; kh < 2; ++kh)
-            tma_load_2d_addr(a_smem + a_buf * (NSEG_A * kASegBytes) + (ia * 2 + kh) * kAHalfBytes, &map_a,
-                             smem_u32(&a_full[a_buf]), ia * kDim + kh * 64, int32_t(row0));
+          for (int kh = 0; kh < KH; ++kh)
+            tma_load_2d_addr(a_smem + a_buf * (NSEG_A * kASegBytes) + (ia * KH + kh) * kAHalfBytes, &map_a,
+                             smem_u32(&a_full[a_buf]), ia * kDim + kh * KBOX, int32_t(row0));
       }
       __syncwarp();
       const uint32_t ngroups = (item.count + kGroupQ - 1) / kGroupQ;
@@ -287,6 +294,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             sts_v4(maddr, qrow[0], qrow[1], qrow[2], qrow[3]);
             sts_v4(maddr + 16, qcol[0], qcol[1], qcol[2], qcol[3]);
             sts_u32(maddr + 32, nvalid | (flags << 8) | (valid_rows << 16));
+            if (FP8) sts_u32(maddr + 36, row0);
             const uint32_t wbar = smem_u32(&w_full[ws]);
             mbar_arrive_expect_tx(&w_full[ws], nvalid * kGateRowBytes);
 #pragma unroll
@@ -299,7 +307,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 #pragma unroll
           for (int ib = 0; ib < NSEG_B; ++ib)
 #pragma unroll
-            for (int kh = 0; kh < 2; ++kh) {
+            for (int kh = 0; kh < KH; ++kh) {
               if (ib + kh > 0) {
                 mbar_wait_timed(&b_empty[stage], sph, st_b);
                 __syncwarp();
@@ -314,7 +322,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 #pragma unroll
                   for (uint32_t qi = 0; qi < kGroupQ; ++qi)
                     if (qi < nvalid)
-                      tma_load_2d_addr(dst + qi * kQBoxBytes, &map_b, fbar, ib * kDim + kh * 64,
+                      tma_load_2d_addr(dst + qi * kQBoxBytes, &map_b, fbar, ib * kDim + kh * KBOX,
                                        int32_t(qrow[qi] * kHeads));
                 }
               }
@@ -356,14 +364,14 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       mbar_wait_timed(&t_empty[acc], ((g >> 1) & 1u) ^ 1u, st_te);
       __syncwarp();
       tc_fence_after();
-      const uint32_t idesc = umma_idesc_bf16(kTileRows, nvalid * kHeads);
+      const uint32_t idesc = FP8 ? umma_idesc_e4m3(kTileRows, nvalid * kHeads) : umma_idesc_bf16(kTileRows, nvalid * kHeads);
       const uint32_t d_tmem = tmem_base + acc * kAccCols;
       const uint64_t a_desc = a_desc0 + uint64_t(a_buf * (NSEG_A * kASegBytes >> 4));
       bool first = true;
 #pragma unroll
       for (int ib = 0; ib < NSEG_B; ++ib)
 #pragma unroll
-        for (int kh = 0; kh < 2; ++kh) {
+        for (int kh = 0; kh < KH; ++kh) {
           if (ib + kh > 0) {
             mbar_wait_timed(&b_full[stage], sph, st_bf);
             __syncwarp();
@@ -374,16 +382,17 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 #pragma unroll
             for (int ia = 0; ia < NSEG_A; ++ia) {
               if ((TERMS >> (ib * 3 + ia)) & 1u) {
-                const uint64_t a_tile = a_desc + uint64_t((ia * 2 + kh) * (kAHalfBytes >> 4));
+                const uint64_t a_tile = a_desc + uint64_t((ia * KH + kh) * (kAHalfBytes >> 4));
 #pragma unroll
-                for (int k4 = 0; k4 < 4; ++k4) {
-                  umma_bf16(d_tmem, a_tile + 2 * k4, b_desc + 2 * k4, idesc, first ? 0u : 1u);
+                for (int k4 = 0; k4 < 4; ++k4) {  // 32 bytes of K per instruction: 16 bf16 or 32 e4m3
+                  if (FP8) umma_f8(d_tmem, a_tile + 2 * k4, b_desc + 2 * k4, idesc, first ? 0u : 1u);
+                  else umma_bf16(d_tmem, a_tile + 2 * k4, b_desc + 2 * k4, idesc, first ? 0u : 1u);
                   first = false;
                 }
               }
             }
             umma_commit(&b_empty[stage]);  // stage reusable once these MMAs have read it
-            if (ib == NSEG_B - 1 && kh == 1) {
+            if (ib == NSEG_B - 1 && kh == KH - 1) {
               umma_commit(&t_full[acc]);
               if (flags & kFlagLast) umma_commit(&a_empty[a_buf]);
             }
@@ -425,6 +434,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     RowSum f0, f1;
     f0.ok = f1.ok = false;
     f0.dst = f1.dst = nullptr;
+    f0.scale = f1.scale = 1.f;
     for (uint32_t g = 0;; ++g) {
       const uint32_t ws = g % kMetaSlots;
       const uint32_t acc = g & 1u;
@@ -434,6 +444,8 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       if ((word >> 8) & kFlagTerminate) break;
       const uint32_t nvalid = word & 0xFFu;
       const bool row_ok = row < (word >> 16);
+      float kscale = 1.f;
+      if (FP8 && row_ok && a.a_scale) kscale = __ldg(a.a_scale + lds_u32(maddr + 36) + row);
       __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the spin loop
       tc_fence_after();
       const bool act0 = qp < nvalid && !(a.debug_flags & 1u);
@@ -468,6 +480,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         reduce_part<1>(vb, g0, a2, a3);
         f0.dst = a.out + uint64_t(qrows.x) * a.out_stride + qcols.x + row;
         f0.ok = row_ok;
+        f0.scale = kscale;
         f0.step1(a0, a1, a2, a3, b0);
         if (act1) {
           tmem_ld_wait();
@@ -480,6 +493,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           tmem_ld_wait();
           f1.dst = a.out + uint64_t(qrows.y) * a.out_stride + qcols.y + row;
           f1.ok = row_ok;
+          f1.scale = kscale;
         } else {
           f0.step2(b1);
           f0.step3();
@@ -514,12 +528,12 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   if (a.stats && threadIdx.x == 0) atomicAdd(a.stats + kStatCta, (unsigned long long)(clock64() - cta_c0));
 }
 
-template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST>
+template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8 = false>
 int launch_variant(const ScoreArgs& args, const CUtensorMap& map_a, const CUtensorMap& map_b, int num_sms,
                    cudaStream_t stream) {
-  using L = SmemLayout<NSEG_A, ABUF, NST>;
+  using L = SmemLayout<NSEG_A, ABUF, NST, FP8 ? 1 : 2>;
   constexpr size_t smem = L::total + 1024;  // slack for the manual 1024 B alignment
-  auto kern = score_tc_kernel<NSEG_A, NSEG_B, TERMS, ABUF, NST>;
+  auto kern = score_tc_kernel<NSEG_A, NSEG_B, TERMS, ABUF, NST, FP8>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -537,6 +551,11 @@ int launch_score_tc(const ScoreArgs& args, const CUtensorMap& map_a, const CUten
                     cudaStream_t stream) {
   const uint32_t terms = pack_terms(args.terms[0], args.terms[1], args.terms[2]);
   // the segment structure is compiled in; these are the combinations the context produces
+  if (args.fp8) {
+    if (args.nseg_a == 1 && args.nseg_b == 1 && terms == pack_terms(1, 0, 0))
+      return launch_variant<1, 1, pack_terms(1, 0, 0), 2, 5, true>(args, map_a, map_b, num_sms, stream);
+    return -1;
+  }
   if (args.nseg_a == 1 && args.nseg_b == 1 && terms == pack_terms(1, 0, 0))
     return launch_variant<1, 1, pack_terms(1, 0, 0), 2, 4>(args, map_a, map_b, num_sms, stream);
   if (args.nseg_a == 2 && args.nseg_b == 1 && terms == pack_terms(3, 0, 0))

@@ -74,3 +74,16 @@ def compare_selection(oracle, prob, strategy, got, rows, rtol, require_exact=Fal
             bad.append((int(r), "tokens", sorted(gs ^ ws)[:8]))
     assert not bad, f"{len(bad)} rows differ beyond near-ties: {bad[:5]}"
     return exact, near, inter / max(total, 1)
+
+
+def quantize_problem_to_fp8(prob):
+    """fp8 storage: keys are quantised per token, queries per (token, head); the query scale is folded into the
+    gates (exact: a positive scale commutes with the ReLU). The oracle is handed exactly what the GPU multiplies:
+    queries = float(q8) (unscaled), gates = w * q_scale, keys = float(k8) * k_scale (one f32 rounding).
+    Returns (q8, k8, k_scale) and rewrites prob in place."""
+    q8, qs = capi.quantize_e4m3(prob.queries)            # [Q,H,d] -> scales [Q,H]
+    k8, ks = capi.quantize_e4m3(prob.keys)               # [L,d]   -> scales [L]
+    prob.queries = capi.e4m3_bits_to_f32(q8).reshape(prob.queries.shape)
+    prob.gates = (prob.gates.astype(np.float32) * qs.astype(np.float32)).astype(np.float32)
+    prob.keys = (capi.e4m3_bits_to_f32(k8) * ks[:, None].astype(np.float32)).astype(np.float32)
+    return q8, k8, ks.astype(np.float32)

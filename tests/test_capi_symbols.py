@@ -64,3 +64,22 @@ def test_bf16_rounding_helpers():
     back = capi.bf16_bits_to_f32(b)
     assert back[0] == 1.0 and back[1] == 1.0 and back[2] == 1.0078125  # ties-to-even at 1 + 2^-8
     assert np.all(np.abs(back[3] - x[3]) <= 2 ** -7 * abs(x[3]))
+
+
+def test_e4m3_helpers_round_trip_and_rounding():
+    import numpy as np
+    allb = np.arange(256, dtype=np.uint8)
+    vals = capi.e4m3_bits_to_f32(allb)
+    finite = ~np.isnan(vals)
+    assert finite.sum() == 254 and vals[0x7E] == 448.0 and vals[0x01] == 2.0 ** -9 and vals[0x08] == 2.0 ** -6
+    # every representable value encodes to itself (−0 keeps its sign bit)
+    assert np.array_equal(capi.f32_to_e4m3_bits(vals[finite]), allb[finite])
+    # ties to even, saturation, subnormal rounding
+    x = np.float32([1.0625, 1.1875, 500.0, -1000.0, 2.0 ** -10, 3 * 2.0 ** -10, 0.0])
+    got = capi.e4m3_bits_to_f32(capi.f32_to_e4m3_bits(x))
+    assert got.tolist() == [1.0, 1.25, 448.0, -448.0, 0.0, 2 * 2.0 ** -9, 0.0]
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((64, 128)).astype(np.float32)
+    b, sc = capi.quantize_e4m3(a)
+    back = capi.e4m3_bits_to_f32(b) * sc[:, None]
+    assert np.abs(back - a).max() <= np.abs(a).max() * 2.0 ** -4   # 3 mantissa bits: half a step of the top binade

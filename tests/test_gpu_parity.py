@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from paper_2603_28458_b200 import capi
-from tests.gpu_helpers import compare_selection, indexer_for, round_problem_to_bf16
+from tests.gpu_helpers import compare_selection, indexer_for, quantize_problem_to_fp8, round_problem_to_bf16
 
 pytestmark = pytest.mark.gpu
 
@@ -402,3 +402,80 @@ def test_host_buffer_pipeline_equals_single_pass(oracle, strategy, monkeypatch):
     sample = np.arange(0, L, 37)
     _, _, rec = compare_selection(oracle, prob, strategy, res[192], sample, BF16_RTOL)
     assert rec >= 0.999
+
+
+# ------------------------------------------------------------------------------------------ fp8 (e4m3) storage
+FP8_RTOL = 1e-3   # north star: bf16/fp8 scores within 1e-3 relative
+
+
+def test_fp8_pool_and_scores_match_oracle(oracle):
+    L, Q, H, d, B = 900, 96, 64, 128, 128
+    pos = oracle.make_positions(L, Q, "spread")
+    prob = oracle.make_inputs("random", 11, L, pos, H, d, block_size=B, block_budget=8, token_budget=64)
+    q8, k8, ks = quantize_problem_to_fp8(prob)
+    with indexer_for(prob, capi.DTYPE_FP8) as ix:
+        ix.upload_keys(k8[:500], scales=ks[:500], check_finite=True)
+        ix.pool_build()
+        ix.pool_append(k8[500:], scales=ks[500:])            # incremental tail update with scales
+        sums, counts, pooled = ix.pool_read()
+        S = ix.score_tokens(q8, prob.gates, pos)
+        J, ne = ix.score_blocks(q8, prob.gates, pos)
+    osums, ocounts, opooled = oracle.pool_build(prob.keys, B, incremental=True)
+    assert counts.tolist() == ocounts.tolist()
+    assert np.array_equal(sums, osums) and np.array_equal(pooled, opooled)   # same f32 keys, same double adds
+    worst = 0.0
+    for r in range(0, Q, 5):
+        t = int(pos[r])
+        want, _ = oracle.score_tokens(prob, r, np.arange(t + 1))
+        err = np.abs(S[r, :t + 1] - want).max() / np.abs(want).max()
+        worst = max(worst, err)
+        wj = oracle.score_blocks(prob, r)
+        assert ne[r] == len(wj)
+        assert np.abs(J[r, :ne[r]] - wj).max() <= 5e-5 * np.abs(wj).max(), f"row {r} (blocks)"
+    print(f"fp8 token scores: worst relative error vs f64 oracle {worst:.3e}")
+    assert worst <= 5e-5   # e4m3 products are exact in fp32; only the accumulation order differs
+
+
+@pytest.mark.parametrize("tb", [0, 1])
+def test_fp8_lattice_bit_exact(oracle, tb):
+    """Small integers are exact in e4m3: with unit scales the fp8 path must reproduce the oracle's indices exactly,
+    including the tie-break."""
+    L, H, d, B, m, k = 1536, 64, 128, 128, 3, 300
+    pos = np.arange(L, dtype=np.uint32)
+    prob = oracle.make_inputs("lattice", 5 + tb, L, pos, H, d, block_size=B, block_budget=m, token_budget=k, tie_break=tb)
+    q8, k8 = capi.f32_to_e4m3_bits(prob.queries), capi.f32_to_e4m3_bits(prob.keys)
+    assert np.array_equal(capi.e4m3_bits_to_f32(q8).reshape(prob.queries.shape), prob.queries)
+    rows = np.unique(np.concatenate([np.arange(0, L, 11), [0, 1, L - 1, k - 1, k, m * B]]))
+    with indexer_for(prob, capi.DTYPE_FP8) as ix:
+        ix.upload_keys(k8)                                    # no scales: 1.0
+        h = ix.hisa_select(q8, prob.gates, pos)
+        f = ix.dsa_select(q8, prob.gates, pos)
+    compare_selection(oracle, prob, "hisa", h, rows, 0.0, require_exact=True)
+    compare_selection(oracle, prob, "dsa", f, rows, 0.0, require_exact=True)
+
+
+def test_fp8_random_inputs_near_tie_rule(oracle):
+    L = Q = 2048
+    H, d, B, m, k = 64, 128, 128, 4, 256
+    pos = np.arange(Q, dtype=np.uint32)
+    prob = oracle.make_inputs("random", 2, L, pos, H, d, block_size=B, block_budget=m, token_budget=k)
+    q8, k8, ks = quantize_problem_to_fp8(prob)
+    with indexer_for(prob, capi.DTYPE_FP8) as ix:
+        ix.upload_keys(k8, scales=ks)
+        h = ix.hisa_select(q8, prob.gates, pos)
+        f = ix.dsa_select(q8, prob.gates, pos)
+    rows = np.arange(Q)
+    ex_h, near_h, rec_h = compare_selection(oracle, prob, "hisa", h, rows, FP8_RTOL)
+    ex_f, near_f, rec_f = compare_selection(oracle, prob, "dsa", f, rows, FP8_RTOL)
+    print(f"fp8 hisa exact={ex_h} near-tie={near_h} recall={rec_h:.6f}; dsa exact={ex_f} near-tie={near_f} recall={rec_f:.6f}")
+    assert rec_h >= 0.999 and rec_f >= 0.999
+    assert ex_h + near_h == Q and ex_f + near_f == Q
+
+
+def test_fp8_rejects_unsupported_shapes():
+    with pytest.raises(capi.HisaError) as e:
+        capi.Indexer(capi.make_config(128, 4, 64, 8, 128, capi.DTYPE_FP8))
+    assert e.value.name == "Unsupported"
+    with pytest.raises(capi.HisaError) as e:
+        capi.Indexer(capi.make_config(128, 4, 64, 64, 128, capi.DTYPE_FP8, scorer=capi.SCORER_SIMT))
+    assert e.value.name == "Unsupported"
