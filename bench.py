@@ -232,7 +232,7 @@ def run_b200(a, rank, world, local_rank):
     def step_flat():
         ix.dsa_select_raw(q.data_ptr(), w.data_ptr(), pos.data_ptr(), nq, out_idx.data_ptr(), out_count.data_ptr(), None)
 
-    def timed(fn, steps, warmup, profile=False):
+    def timed(fn, steps, warmup, profile=False, stall_stats=False):
         for _ in range(warmup):
             fn()
         ix.synchronize()
@@ -240,8 +240,10 @@ def run_b200(a, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
         if profile:
-            ix.set_profiling(True)
+            ix.set_profiling(True, stall_stats=stall_stats)
             ix.stage_times()  # reset accumulators
+            if stall_stats:
+                ix.scorer_stall_cycles()
         l0 = ix.launch_count()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
@@ -255,7 +257,7 @@ def run_b200(a, rank, world, local_rank):
         ms = e0.elapsed_time(e1)
         stages = ix.stage_times() if profile else None
         if profile:
-            stages["stalls"] = ix.scorer_stall_cycles()
+            stages["stalls"] = ix.scorer_stall_cycles() if stall_stats else None
             ix.set_profiling(False)
         launches = ix.launch_count() - l0
         if dist:
@@ -297,13 +299,15 @@ def run_b200(a, rank, world, local_rank):
                 "flops_per_launch": flops_s2, "kernel_ms": k_ms}
     per_call = {kk: (vv / max(stages["calls"], 1) if kk.endswith("_ms") else vv) for kk, vv in stages.items()
                 if kk != "stalls"}
+    # role-level stall accounting: a short separate pass with the instrumented scorer instantiation (not timed)
+    _, st_stages, _ = timed(step_hisa, min(a.steps, 3), 0, profile=True, stall_stats=True)
     stalls = {}
-    for st_name, st in stages["stalls"].items():
+    for st_name, st in st_stages["stalls"].items():
         cta = max(st["cta"], 1)
         stalls[st_name] = {kk: (round(vv / cta, 4) if kk != "groups" else vv) for kk, vv in st.items()
                            if kk != "cta" and not kk.startswith("epi_")}
         # SM clock the kernel really ran at: CTA lifetime cycles (one persistent CTA per SM) / its CUDA-event time
-        st_ms = stages["score_blocks_ms" if st_name == "stage1" else "score_tokens_ms"]
+        st_ms = st_stages["score_blocks_ms" if st_name == "stage1" else "score_tokens_ms"]
         if st_ms > 0:
             n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
             stalls[st_name]["sm_mhz_in_kernel"] = round(st["cta"] / n_sm / (st_ms * 1e-3) / 1e6, 1)

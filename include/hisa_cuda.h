@@ -198,7 +198,9 @@ typedef struct hisa_cuda_stage_times {
   uint64_t work_items_stage1, work_items_stage2; /* scorer work-item capacity (tile x query-list units) */
   uint64_t calls;        /* API calls accumulated in this record */
 } hisa_cuda_stage_times;
-/* enable != 0: record CUDA events around every stage of subsequent calls (adds a few us). */
+/* enable != 0: record CUDA events around every stage of subsequent calls (adds a few us).
+ * enable & 2: additionally launch the instrumented instantiation of the tensor-core scorer, which keeps the role-level
+ * stall counters read by hisa_cuda_scorer_stall_cycles (its clock reads slow the kernel down by a few percent). */
 int hisa_cuda_set_profiling(hisa_cuda_ctx* ctx, int enable);
 /* Sums over all calls since the previous read (then resets); synchronizes the context's stream. */
 int hisa_cuda_last_stage_times(hisa_cuda_ctx* ctx, hisa_cuda_stage_times* out);

@@ -228,7 +228,9 @@ class Indexer:
         return np.ascontiguousarray(a, dtype=np.float32)
 
     def synchronize(self): _check(lib().hisa_cuda_synchronize(self._ctx), self._ctx)
-    def set_profiling(self, on: bool): _check(lib().hisa_cuda_set_profiling(self._ctx, C.c_int(int(on))), self._ctx)
+    def set_profiling(self, on, stall_stats: bool = False):
+        """on: CUDA events per stage; stall_stats: also run the instrumented scorer (slower by a few percent)."""
+        _check(lib().hisa_cuda_set_profiling(self._ctx, C.c_int((1 if on else 0) | (2 if (on and stall_stats) else 0))), self._ctx)
 
     def stage_times(self) -> dict:
         st = StageTimes()
@@ -236,7 +238,7 @@ class Indexer:
         return st.as_dict()
 
     STALL_NAMES = ["cta", "prod_wait_sched", "prod_wait_tilebuf", "prod_wait_qstage", "mma_wait_qdata", "mma_wait_tile",
-                   "mma_wait_epilogue", "epi_wait_gates", "epi_wait_mma", "epi_busy", "groups"]
+                   "mma_wait_epilogue", "mma_wait_gates", "epi_wait_mma", "epi_busy", "groups"]
 
     def scorer_stall_cycles(self) -> dict:
         a, b = (C.c_uint64 * 16)(), (C.c_uint64 * 16)()

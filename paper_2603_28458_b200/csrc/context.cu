@@ -66,7 +66,8 @@ struct hisa_cuda_ctx {
   uint64_t workspace_bytes = 4ull << 30;
 
   // instrumentation
-  bool profiling = false;
+  bool profiling = false;    // CUDA events around every stage
+  bool stall_stats = false;  // additionally run the instrumented scorer instantiation (role-level stall cycles)
   std::vector<StageSpan> spans;
   std::vector<cudaEvent_t> event_pool;
   size_t events_used = 0;
@@ -355,7 +356,7 @@ int run_scorer(hisa_cuda_ctx* ctx, const ScoreJob& j) {
   a.a_scale = j.a_scale;
   a.debug_flags = env_u32("HISA_TC_DEBUG", 0);
   a.stats = nullptr;
-  if (ctx->profiling) {
+  if (ctx->profiling && ctx->stall_stats) {
     if (!ctx->stats.p) {
       HISA_TRY(ensure(ctx, ctx->stats, 2 * 16 * sizeof(unsigned long long)));
       CU_TRY(ctx, cudaMemsetAsync(ctx->stats.p, 0, 2 * 16 * sizeof(unsigned long long), ctx->stream));
@@ -1321,6 +1322,7 @@ int hisa_cuda_score_tokens(hisa_cuda_ctx* ctx, const void* queries, const float*
 int hisa_cuda_set_profiling(hisa_cuda_ctx* ctx, int enable) {
   if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
   ctx->profiling = enable != 0;
+  ctx->stall_stats = (enable & 2) != 0;
   return HISA_OK;
 }
 

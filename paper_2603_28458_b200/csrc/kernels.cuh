@@ -66,7 +66,7 @@ enum ScoreStat : int {
   kStatMmaBFull,         // MMA issuer waiting for query data (TMA latency / bandwidth)
   kStatMmaAFull,         // MMA issuer waiting for tile data
   kStatMmaTEmpty,        // MMA issuer waiting for the epilogue to drain an accumulator
-  kStatEpiWFull,         // epilogue (warp 0) waiting for gates/meta
+  kStatEpiWFull,         // MMA issuer waiting for the gates of a group (they ride with its first query chunk)
   kStatEpiTFull,         // epilogue (warp 0) waiting for the MMA
   kStatEpiBusy,          // epilogue (warp 0) cycles between t_full and t_empty arrive
   kStatGroups,           // groups processed

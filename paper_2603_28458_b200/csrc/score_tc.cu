@@ -28,10 +28,12 @@
 //     the issuing thread keeps up, so the issue loop is written to be lean: warp-uniform control flow (all
 //     lanes wait, one elected lane issues), descriptors built by adding constants to per-stage bases.
 //
-// Warp roles (352 threads): warps 0-7 epilogue (warp%4 = TMEM lane quarter, warp/4 = which PAIR of the 4 queries),
-// warp 8 TMA producer, warp 9 MMA issuer + TMEM owner, warp 10 scheduler. Eight fat epilogue warps (up to 184
-// registers) instead of sixteen thin ones: the fixed per-group cost of an epilogue warp (barrier wait, meta reads,
-// output address, shuffles) is paid half as often, and each warp keeps a tcgen05.ld in flight under its own math.
+// Warp roles (608 threads): warps 0-15 epilogue in two sets of eight (set = warp / 8 takes the groups with
+// g % 2 == set, i.e. it owns one of the two TMEM accumulators; inside a set warp % 4 = TMEM lane quarter and
+// (warp / 4) % 2 = which PAIR of the group's 4 queries), warp 16 TMA producer, warp 17 MMA issuer + TMEM owner,
+// warp 18 scheduler. With the sets half a period apart each SM sub-partition always has warps of both sets to issue
+// from (tcgen05.ld / LDS / shuffle latencies of one set hide under the FMNMX/FFMA2 stream of the other), and every
+// warp additionally keeps one 16-register tcgen05.ld in flight under its own math.
 #include "kernels.cuh"
 #include "ptx.cuh"
 
@@ -39,11 +41,12 @@ namespace hisa_dev {
 
 namespace {
 
-constexpr int kEpiWarps = 8;
-constexpr int kProducerWarp = 8;
-constexpr int kMmaWarp = 9;
-constexpr int kSchedWarp = 10;
-constexpr int kTcThreads = 11 * 32;
+constexpr int kEpiWarps = 16;
+constexpr int kEpiSetWarps = 8;  // epilogue warps per accumulator
+constexpr int kProducerWarp = 16;
+constexpr int kMmaWarp = 17;
+constexpr int kSchedWarp = 18;
+constexpr int kTcThreads = 19 * 32;
 constexpr int kMetaSlots = 8;
 constexpr int kUnitSlots = 4;
 constexpr uint32_t kAHalfBytes = kTileRows * 128;      // one 64-element K-half of one A segment: 16 KB
@@ -72,8 +75,8 @@ struct SmemLayout {
   static constexpr uint32_t meta_off = w_off + kMetaSlots * kGroupQ * kGateRowBytes;
   static constexpr uint32_t unit_off = meta_off + kMetaSlots * sizeof(GroupMeta);
   static constexpr uint32_t bar_off = unit_off + kUnitSlots * sizeof(WorkItem);
-  // barriers: b_full[NST] b_empty[NST] a_full[ABUF] a_empty[ABUF] t_full[2] t_empty[2] w_full[8] u_full[4] u_empty[4]
-  static constexpr uint32_t num_bars = 2 * NST + 2 * ABUF + 4 + kMetaSlots + 2 * kUnitSlots;
+  // barriers: b_full[NST] b_empty[NST] a_full[ABUF] a_empty[ABUF] t_full[2] t_empty[2] u_full[4] u_empty[4]
+  static constexpr uint32_t num_bars = 2 * NST + 2 * ABUF + 4 + 2 * kUnitSlots;
   static constexpr uint32_t tmem_off = bar_off + num_bars * 8;
   static constexpr uint32_t total = tmem_off + 16;
 };
@@ -94,35 +97,25 @@ __device__ __forceinline__ void ffma2(float2& acc, float a0, float a1, float b0,
   asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(cv));
 }
 
-// gate * relu head reduction over part of ONE tcgen05.ld.16x128b.x16 fragment (see ptx.cuh): the lane holds heads
-// {4i + c : i = 0..15} of two key rows; gw[] are its 16 permuted gates (4 x LDS.128, loaded once per query and used
-// for both halves). PART selects heads i in [8 PART, 8 PART + 8): each gate pair feeds two packed FMAs, one per row.
-template <int PART>
-__device__ __forceinline__ void reduce_part(const uint32_t (&v)[32], const float4 (&gw)[4], float2& a0, float2& a1) {
+// gate * relu head reduction over ONE tcgen05.ld.16x128b.x8 fragment (16 lanes x 32 columns, see ptx.cuh): the lane
+// holds heads {32 CH + 4i + c : i = 0..7} of two key rows; g0, g1 are the 8 permuted gates of those heads. Each gate
+// pair feeds two packed FMAs, one per row.
+__device__ __forceinline__ void reduce_frag(const uint32_t (&v)[16], const float4& g0, const float4& g1, float2& a0,
+                                            float2& a1) {
 #pragma unroll
-  for (int h = 2 * PART; h < 2 * PART + 2; ++h) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int i = 2 * h + e;  // heads 8i + c and 8i + 4 + c
-      const float wx = e ? gw[h].z : gw[h].x, wy = e ? gw[h].w : gw[h].y;
-      ffma2(a0, wx, wy, fmaxf(__uint_as_float(v[4 * i + 0]), 0.f), fmaxf(__uint_as_float(v[4 * i + 2]), 0.f));
-      ffma2(a1, wx, wy, fmaxf(__uint_as_float(v[4 * i + 1]), 0.f), fmaxf(__uint_as_float(v[4 * i + 3]), 0.f));
-    }
+  for (int i = 0; i < 4; ++i) {  // heads 8i + c and 8i + 4 + c of this column half
+    const float4& gq = i < 2 ? g0 : g1;
+    const float wx = (i & 1) ? gq.z : gq.x, wy = (i & 1) ? gq.w : gq.y;
+    ffma2(a0, wx, wy, fmaxf(__uint_as_float(v[4 * i + 0]), 0.f), fmaxf(__uint_as_float(v[4 * i + 2]), 0.f));
+    ffma2(a1, wx, wy, fmaxf(__uint_as_float(v[4 * i + 1]), 0.f), fmaxf(__uint_as_float(v[4 * i + 3]), 0.f));
   }
-}
-__device__ __forceinline__ void load_gates(float4 (&gw)[4], uint32_t waddr) {
-#pragma unroll
-  for (int h = 0; h < 4; ++h) gw[h] = lds_f4(waddr + h * 16);
 }
 
 // Transposed butterfly over the 4 lanes that share key rows: each lane enters with its partial sums of four rows and
 // leaves with the full sum of row slot (lane & 3). Split into three steps so that the two shuffle latencies can be
-// covered by the reduction of the next half-fragment.
+// covered by the reduction of the next fragment.
 struct RowSum {
   float keep0, keep1, got0, got1;
-  float scale;  // per-key dequantisation scale (fp8 operands), 1 otherwise
-  float* dst;
-  bool ok;
   __device__ __forceinline__ void step1(const float2& a0, const float2& a1, const float2& a2, const float2& a3, bool b0) {
     const float s0 = a0.x + a0.y, s1 = a1.x + a1.y, s2 = a2.x + a2.y, s3 = a3.x + a3.y;
     keep0 = b0 ? s1 : s0;
@@ -135,9 +128,7 @@ struct RowSum {
     keep0 = b1 ? k1 : k0;
     got0 = __shfl_xor_sync(0xffffffffu, b1 ? k0 : k1, 2);
   }
-  __device__ __forceinline__ void step3() {
-    if (ok) *dst = (keep0 + got0) * scale;
-  }
+  __device__ __forceinline__ float result() const { return keep0 + got0; }
 };
 
 // TERMS: bit (ib * 3 + ia) set <=> A segment ia is multiplied with B segment ib
@@ -145,7 +136,7 @@ struct RowSum {
 // row, so a segment is a single K slab (KH = 1) where bf16 needs two (KH = 2), and a group needs one 32 KB query
 // chunk instead of two; the per-key dequantisation scale multiplies the finished row sum (scale > 0 commutes with
 // the ReLU), the per-(query, head) scale is part of the gate.
-template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8>
+template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8, bool STATS>
 __global__ void __launch_bounds__(kTcThreads, 1)
 score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, ScoreArgs a) {
   constexpr int KH = FP8 ? 1 : 2;                     // 128-byte K slabs per operand segment
@@ -168,20 +159,25 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   uint64_t* a_empty = a_full + ABUF;
   uint64_t* t_full = a_empty + ABUF;
   uint64_t* t_empty = t_full + 2;
-  uint64_t* w_full = t_empty + 2;
-  uint64_t* u_full = w_full + kMetaSlots;
+  uint64_t* u_full = t_empty + 2;
   uint64_t* u_empty = u_full + kUnitSlots;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::tmem_off);
 
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
-  const long long cta_c0 = clock64();
+  const long long cta_c0 = STATS ? clock64() : 0;
+  // role-level stall accounting only exists in the STATS instantiation (profiling on): the clock reads around every
+  // wait cost the MMA warp tens of cycles per group, and tools/umma_queue_bench.cu shows the tensor pipe drains its
+  // queue ~150-250 cycles after the issuing thread stops feeding it
+  auto wait_timed = [&](uint64_t* bar, uint32_t parity, uint64_t& acc_cycles) {
+    if (STATS) mbar_wait_timed(bar, parity, acc_cycles);
+    else mbar_wait(bar, parity);
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
     for (int i = 0; i < ABUF; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&t_full[i], 1); mbar_init(&t_empty[i], kEpiWarps); }
-    for (int i = 0; i < kMetaSlots; ++i) mbar_init(&w_full[i], 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&t_full[i], 1); mbar_init(&t_empty[i], kEpiSetWarps); }
     for (int i = 0; i < kUnitSlots; ++i) { mbar_init(&u_full[i], 1); mbar_init(&u_empty[i], 1); }
     fence_barrier_init();
     fence_proxy_async();
@@ -227,17 +223,18 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     const uint32_t a_smem = smem_u32(s_a), b_smem = smem_u32(s_b), w_smem = smem_u32(s_w);
     for (uint32_t useq = 0;; ++useq) {
       const uint32_t slot = useq % kUnitSlots;
-      mbar_wait_timed(&u_full[slot], (useq / kUnitSlots) & 1u, st_unit);
+      wait_timed(&u_full[slot], (useq / kUnitSlots) & 1u, st_unit);
       const WorkItem item = s_unit[slot];
       __syncwarp();
       if (lane == 0) mbar_arrive(&u_empty[slot]);
       if (item.count == 0) {
         if (lane == 0) {
           mbar_wait(&b_empty[stage], sph);
+          // both epilogue sets must see the marker: the set of group g reads slot ws, the other one slot ws + 1
           sts_u32(meta_base + ws * uint32_t(sizeof(GroupMeta)) + 32, kFlagTerminate << 8);
-          mbar_arrive(&w_full[ws]);
+          sts_u32(meta_base + ((ws + 1) % kMetaSlots) * uint32_t(sizeof(GroupMeta)) + 32, kFlagTerminate << 8);
           mbar_arrive(&b_full[stage]);
-          if (a.stats) {
+          if (STATS && a.stats) {
             atomicAdd(a.stats + kStatProdUnit, st_unit);
             atomicAdd(a.stats + kStatProdAEmpty, st_a);
             atomicAdd(a.stats + kStatProdBEmpty, st_b);
@@ -249,7 +246,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const uint32_t row0 = tile_row0(a, item.tile);
       const uint32_t valid_rows = tile_valid_rows(a, item.tile);
       const uint32_t col_add = a.list_mode ? (item.tile % a.segs_per_block) * kTileRows : item.tile * kTileRows;
-      mbar_wait_timed(&a_empty[a_buf], ((useq / ABUF) & 1u) ^ 1u, st_a);
+      wait_timed(&a_empty[a_buf], ((useq / ABUF) & 1u) ^ 1u, st_a);
       __syncwarp();
       if (elect_one()) {
         mbar_arrive_expect_tx(&a_full[a_buf], NSEG_A * kASegBytes);
@@ -287,7 +284,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           const uint32_t gg = gb + gi;
           const uint32_t nvalid = min(uint32_t(kGroupQ), item.count - gg * kGroupQ);
           const uint32_t flags = (gg == 0 ? kFlagFirst : 0u) | (gg + 1 == ngroups ? kFlagLast : 0u);
-          mbar_wait_timed(&b_empty[stage], sph, st_b);  // first chunk of the group: also guards the meta/gate slot
+          wait_timed(&b_empty[stage], sph, st_b);  // first chunk of the group: also guards the meta/gate slot
           __syncwarp();
           if (elect_one()) {
             const uint32_t maddr = meta_base + ws * uint32_t(sizeof(GroupMeta));
@@ -295,11 +292,12 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             sts_v4(maddr + 16, qcol[0], qcol[1], qcol[2], qcol[3]);
             sts_u32(maddr + 32, nvalid | (flags << 8) | (valid_rows << 16));
             if (FP8) sts_u32(maddr + 36, row0);
-            const uint32_t wbar = smem_u32(&w_full[ws]);
-            mbar_arrive_expect_tx(&w_full[ws], nvalid * kGateRowBytes);
+            // the gates ride on the barrier of the group's first query chunk (one wait for the MMA warp; the epilogue
+            // sees them through t_full)
+            const uint32_t wbar = smem_u32(&b_full[stage]);
 #pragma unroll
             for (uint32_t qi = 0; qi < kGroupQ; ++qi)
-              if (qi < nvalid)
+              if (qi < nvalid && !(a.debug_flags & 4u))
                 bulk_load_1d_addr(w_smem + (ws * kGroupQ + qi) * kGateRowBytes, a.gates + uint64_t(qrow[qi]) * kHeads,
                                   kGateRowBytes, wbar);
           }
@@ -309,15 +307,16 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 #pragma unroll
             for (int kh = 0; kh < KH; ++kh) {
               if (ib + kh > 0) {
-                mbar_wait_timed(&b_empty[stage], sph, st_b);
+                wait_timed(&b_empty[stage], sph, st_b);
                 __syncwarp();
               }
               if (elect_one()) {
                 const uint32_t fbar = smem_u32(&b_full[stage]);
+                const uint32_t gate_bytes = (ib + kh == 0 && !(a.debug_flags & 4u)) ? nvalid * kGateRowBytes : 0u;
                 if (a.debug_flags & 2u) {
-                  mbar_arrive(&b_full[stage]);
+                  mbar_arrive_expect_tx(&b_full[stage], gate_bytes);
                 } else {
-                  mbar_arrive_expect_tx(&b_full[stage], nvalid * kQBoxBytes);
+                  mbar_arrive_expect_tx(&b_full[stage], nvalid * kQBoxBytes + gate_bytes);
                   const uint32_t dst = b_smem + stage * kBChunkBytes;
 #pragma unroll
                   for (uint32_t qi = 0; qi < kGroupQ; ++qi)
@@ -345,23 +344,24 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     const uint64_t a_desc0 = umma_smem_desc_sw128(smem_u32(s_a));
     const uint64_t b_desc0 = umma_smem_desc_sw128(smem_u32(s_b));
     for (;;) {
-      mbar_wait_timed(&b_full[stage], sph, st_bf);
+      wait_timed(&b_full[stage], sph, st_bf);
       const uint32_t word = lds_u32(meta_base + ws * uint32_t(sizeof(GroupMeta)) + 32);
       const uint32_t flags = (word >> 8) & 0xFFu;
       const uint32_t acc = g & 1u;
       if (flags & kFlagTerminate) {
-        // the epilogue only watches t_full: pass the terminate marker on through it
+        // the epilogue only watches t_full: pass the terminate marker on through it, to both sets
         mbar_wait(&t_empty[acc], ((g >> 1) & 1u) ^ 1u);
-        if (lane == 0) mbar_arrive(&t_full[acc]);
+        mbar_wait(&t_empty[acc ^ 1u], (((g + 1) >> 1) & 1u) ^ 1u);
+        if (lane == 0) {
+          mbar_arrive(&t_full[acc]);
+          mbar_arrive(&t_full[acc ^ 1u]);
+        }
         break;
       }
       const uint32_t nvalid = word & 0xFFu;
       const uint32_t a_buf = units % ABUF;  // same sequence as the producer's useq % ABUF
-      if (flags & kFlagFirst) mbar_wait_timed(&a_full[a_buf], (units / ABUF) & 1u, st_af);
-      // gates of the group have landed (issued before its first query chunk): t_full then covers them as well, and
-      // the epilogue warps wait on a single barrier per group
-      mbar_wait_timed(&w_full[ws], (g / kMetaSlots) & 1u, st_bf);
-      mbar_wait_timed(&t_empty[acc], ((g >> 1) & 1u) ^ 1u, st_te);
+      if (flags & kFlagFirst) wait_timed(&a_full[a_buf], (units / ABUF) & 1u, st_af);
+      wait_timed(&t_empty[acc], ((g >> 1) & 1u) ^ 1u, st_te);
       __syncwarp();
       tc_fence_after();
       const uint32_t idesc = FP8 ? umma_idesc_e4m3(kTileRows, nvalid * kHeads) : umma_idesc_bf16(kTileRows, nvalid * kHeads);
@@ -373,7 +373,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 #pragma unroll
         for (int kh = 0; kh < KH; ++kh) {
           if (ib + kh > 0) {
-            mbar_wait_timed(&b_full[stage], sph, st_bf);
+            wait_timed(&b_full[stage], sph, st_bf);
             __syncwarp();
             tc_fence_after();
           }
@@ -405,7 +405,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       ws = (ws + 1) % kMetaSlots;
       ++g;
     }
-    if (a.stats && lane == 0) {
+    if (STATS && a.stats && lane == 0) {
       atomicAdd(a.stats + kStatMmaBFull, st_bf);
       atomicAdd(a.stats + kStatMmaAFull, st_af);
       atomicAdd(a.stats + kStatMmaTEmpty, st_te);
@@ -413,32 +413,26 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     }
   } else if (warp < kEpiWarps) {
     // ================= epilogue: TMEM -> gate*ReLU head reduction -> HBM =================
-    // Each warp reduces a 32-row quarter of the tile for TWO queries of the group = four half-fragments of 32
-    // registers (tcgen05.ld.16x128b.x16), software-pipelined through two register buffers: the load of the next half
-    // is in flight while the FMNMX/FFMA2 work of the current one issues, and the last half of group g is reduced
-    // under the first load of group g+1 (the accumulator is handed back as soon as all four loads have landed).
-    // Fragment layout (tcgen05.ld.16x128b, twice the TMEM read rate of 16x256b): a lane owns 16 of the 64 heads for two key rows per half, so it needs
-    // only 16 gates (64 B) per query instead of all 64: the gate traffic through the 128 B/clk shared-memory return
-    // path is what bounded a one-row-per-thread (32x32b) epilogue. The 4 lanes sharing a row are summed by shuffles.
+    // A warp reduces a 32-row quarter of the tile for TWO queries of every second group: eight fragments
+    // F(query, row half, column half) of 16 registers (tcgen05.ld.16x128b.x8), streamed through two register buffers
+    // so that the load of fragment i+1 is in flight while the FMNMX/FFMA2 work of fragment i issues. The accumulator
+    // goes back to the MMA warp as soon as the eighth load has landed.
+    // Fragment layout (tcgen05.ld.16x128b, twice the TMEM read rate of 16x256b): a lane owns 16 of the 64 heads for
+    // two key rows per row half, so it needs only 16 gates (64 B) per query instead of all 64: the gate traffic
+    // through the 128 B/clk shared-memory return path is what bounded a one-row-per-thread (32x32b) epilogue. The 4
+    // lanes sharing a row are summed by shuffles.
+    const uint32_t set = warp >> 3;        // accumulator / group parity this warp serves
     const uint32_t quarter = warp & 3u;
-    const uint32_t qp = (warp >> 2) * 2u;  // first of the two queries this warp reduces
+    const uint32_t qp = ((warp >> 2) & 1u) * 2u;  // first of the two queries this warp reduces
     const uint32_t w_lane = smem_u32(s_w) + qp * kGateRowBytes + (lane & 3u) * 64u;
-    const uint32_t t_lane = tmem_base + ((quarter * 32u) << 16) + qp * kHeads;
+    const uint32_t t_lane = tmem_base + ((quarter * 32u) << 16) + set * kAccCols + qp * kHeads;
     const uint32_t row = quarter * 32 + (lane >> 2) + 8u * (lane & 3u);
     const bool b0 = lane & 1u, b1 = lane & 2u;
-    const uint32_t t_full_addr = smem_u32(t_full), t_empty_addr = smem_u32(t_empty);
-    uint32_t va[32], vb[32];
-    float4 g0[4], g1[4];                         // gates of the warp's two queries (this lane's 16 heads each)
-    float2 c0 = make_float2(0.f, 0.f), c1 = c0;  // first-half sums of the deferred (second) query
-    bool pend = false;                           // its second half (in vb) still has to be reduced and stored
-    RowSum f0, f1;
-    f0.ok = f1.ok = false;
-    f0.dst = f1.dst = nullptr;
-    f0.scale = f1.scale = 1.f;
-    for (uint32_t g = 0;; ++g) {
+    const uint32_t t_full_addr = smem_u32(&t_full[set]), t_empty_addr = smem_u32(&t_empty[set]);
+    uint32_t vx[16], vy[16];
+    for (uint32_t g = set;; g += 2) {
       const uint32_t ws = g % kMetaSlots;
-      const uint32_t acc = g & 1u;
-      mbar_wait_addr(t_full_addr + acc * 8, (g >> 1) & 1u);
+      mbar_wait_addr(t_full_addr, (g >> 1) & 1u);
       const uint32_t maddr = meta_base + ws * uint32_t(sizeof(GroupMeta));
       const uint32_t word = lds_u32(maddr + 32);
       if ((word >> 8) & kFlagTerminate) break;
@@ -450,71 +444,65 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       tc_fence_after();
       const bool act0 = qp < nvalid && !(a.debug_flags & 1u);
       const bool act1 = qp + 1 < nvalid && !(a.debug_flags & 1u);
-      const uint32_t taddr = t_lane + acc * kAccCols;
       const uint32_t waddr = w_lane + ws * (kGroupQ * kGateRowBytes);
       if (act0) {
-        tmem_ld_16x128b_x16(taddr, va);  // query 0, rows quarter*32 + {T/4, T/4 + 8}
-        load_gates(g0, waddr);
-      }
-      float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
-      if (pend) {  // previous group's last half (query 1, rows + 16), under the load just issued
-        reduce_part<0>(vb, g1, a2, a3);
-        reduce_part<1>(vb, g1, a2, a3);
-        f1.step1(c0, c1, a2, a3, b0);
-        a2 = a3 = make_float2(0.f, 0.f);
-      }
-      if (act0) {
+        // fragment address: + 32 per column half, + 16 lanes per row half, + 64 columns for the second query
+        tmem_ld_16x128b_x8(t_lane, vx);                                // F(0, 0, 0)
+        float4 gw[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) gw[h] = lds_f4(waddr + h * 16);
         const uint2 qrows = lds_u2(maddr + qp * 4), qcols = lds_u2(maddr + 16 + qp * 4);
+        float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+        RowSum f;
         tmem_ld_wait();
-        tmem_ld_16x128b_x16(taddr + (16u << 16), vb);  // query 0, rows + 16
-        reduce_part<0>(va, g0, a0, a1);
-        if (pend) f1.step2(b1);
-        reduce_part<1>(va, g0, a0, a1);
-        if (pend) f1.step3();
+        tmem_ld_16x128b_x8(t_lane + 32, vy);                           // F(0, 0, 1)
+        reduce_frag(vx, gw[0], gw[1], a0, a1);
         tmem_ld_wait();
+        tmem_ld_16x128b_x8(t_lane + (16u << 16), vx);                  // F(0, 1, 0)
+        reduce_frag(vy, gw[2], gw[3], a0, a1);
+        tmem_ld_wait();
+        tmem_ld_16x128b_x8(t_lane + (16u << 16) + 32, vy);             // F(0, 1, 1)
+        reduce_frag(vx, gw[0], gw[1], a2, a3);
+        tmem_ld_wait();
+        if (act1) tmem_ld_16x128b_x8(t_lane + kHeads, vx);             // F(1, 0, 0)
+        reduce_frag(vy, gw[2], gw[3], a2, a3);
+        f.step1(a0, a1, a2, a3, b0);
+        float* dst0 = a.out + uint64_t(qrows.x) * a.out_stride + qcols.x + row;
         if (act1) {
-          tmem_ld_16x128b_x16(taddr + kHeads, va);  // query 1, first half
-          load_gates(g1, waddr + kGateRowBytes);
-        }
-        reduce_part<0>(vb, g0, a2, a3);
-        reduce_part<1>(vb, g0, a2, a3);
-        f0.dst = a.out + uint64_t(qrows.x) * a.out_stride + qcols.x + row;
-        f0.ok = row_ok;
-        f0.scale = kscale;
-        f0.step1(a0, a1, a2, a3, b0);
-        if (act1) {
+#pragma unroll
+          for (int h = 0; h < 4; ++h) gw[h] = lds_f4(waddr + kGateRowBytes + h * 16);
+          a0 = a1 = a2 = a3 = make_float2(0.f, 0.f);
           tmem_ld_wait();
-          tmem_ld_16x128b_x16(taddr + kHeads + (16u << 16), vb);  // query 1, rows + 16: reduced in the next iteration
-          c0 = c1 = make_float2(0.f, 0.f);
-          reduce_part<0>(va, g1, c0, c1);
-          f0.step2(b1);
-          reduce_part<1>(va, g1, c0, c1);
-          f0.step3();
+          tmem_ld_16x128b_x8(t_lane + kHeads + 32, vy);                // F(1, 0, 1)
+          f.step2(b1);
+          reduce_frag(vx, gw[0], gw[1], a0, a1);
           tmem_ld_wait();
-          f1.dst = a.out + uint64_t(qrows.y) * a.out_stride + qcols.y + row;
-          f1.ok = row_ok;
-          f1.scale = kscale;
+          tmem_ld_16x128b_x8(t_lane + kHeads + (16u << 16), vx);       // F(1, 1, 0)
+          if (row_ok) *dst0 = f.result() * kscale;
+          reduce_frag(vy, gw[2], gw[3], a0, a1);
+          tmem_ld_wait();
+          tmem_ld_16x128b_x8(t_lane + kHeads + (16u << 16) + 32, vy);  // F(1, 1, 1)
+          reduce_frag(vx, gw[0], gw[1], a2, a3);
+          tmem_ld_wait();
         } else {
-          f0.step2(b1);
-          f0.step3();
+          f.step2(b1);
+          if (row_ok) *dst0 = f.result() * kscale;
         }
-      } else if (pend) {
-        f1.step2(b1);
-        f1.step3();
+        // all dots of the group are in registers: hand the accumulator back to the MMA warp
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_addr(t_empty_addr);
+        if (act1) {
+          reduce_frag(vy, gw[2], gw[3], a2, a3);
+          f.step1(a0, a1, a2, a3, b0);
+          f.step2(b1);
+          if (row_ok) a.out[uint64_t(qrows.y) * a.out_stride + qcols.y + row] = f.result() * kscale;
+        }
+      } else {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_addr(t_empty_addr);
       }
-      // all dots of the group are in registers: hand the accumulator back to the MMA warp
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_addr(t_empty_addr + acc * 8);
-      pend = act1;
-    }
-    if (pend) {
-      float2 a2 = make_float2(0.f, 0.f), a3 = a2;
-      reduce_part<0>(vb, g1, a2, a3);
-      reduce_part<1>(vb, g1, a2, a3);
-      f1.step1(c0, c1, a2, a3, b0);
-      f1.step2(b1);
-      f1.step3();
     }
   }
 
@@ -525,21 +513,28 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
   }
-  if (a.stats && threadIdx.x == 0) atomicAdd(a.stats + kStatCta, (unsigned long long)(clock64() - cta_c0));
+  if (STATS && a.stats && threadIdx.x == 0) atomicAdd(a.stats + kStatCta, (unsigned long long)(clock64() - cta_c0));
 }
 
-template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8 = false>
-int launch_variant(const ScoreArgs& args, const CUtensorMap& map_a, const CUtensorMap& map_b, int num_sms,
-                   cudaStream_t stream) {
+template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8, bool STATS>
+void launch_instance(const ScoreArgs& args, const CUtensorMap& map_a, const CUtensorMap& map_b, int num_sms,
+                     cudaStream_t stream) {
   using L = SmemLayout<NSEG_A, ABUF, NST, FP8 ? 1 : 2>;
   constexpr size_t smem = L::total + 1024;  // slack for the manual 1024 B alignment
-  auto kern = score_tc_kernel<NSEG_A, NSEG_B, TERMS, ABUF, NST, FP8>;
+  auto kern = score_tc_kernel<NSEG_A, NSEG_B, TERMS, ABUF, NST, FP8, STATS>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     configured = true;
   }
   kern<<<num_sms, kTcThreads, smem, stream>>>(map_a, map_b, args);
+}
+
+template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8 = false>
+int launch_variant(const ScoreArgs& args, const CUtensorMap& map_a, const CUtensorMap& map_b, int num_sms,
+                   cudaStream_t stream) {
+  if (args.stats) launch_instance<NSEG_A, NSEG_B, TERMS, ABUF, NST, FP8, true>(args, map_a, map_b, num_sms, stream);
+  else launch_instance<NSEG_A, NSEG_B, TERMS, ABUF, NST, FP8, false>(args, map_a, map_b, num_sms, stream);
   return 1;
 }
 
