@@ -53,6 +53,7 @@ struct ScoreArgs {
   uint32_t a_rows;             // rows that exist in the A operand (rows beyond read as zero)
   uint32_t fp8;                // operands are e4m3 bytes [rows, 128] (kind::f8f6f4); nseg_a = nseg_b = 1
   const float* a_scale;        // fp8: per-row dequantisation scale of the A operand (may be null = 1)
+  uint32_t producers;          // TMA producer warps that take part (1..3)
   uint32_t debug_flags;        // timing experiments only (HISA_TC_DEBUG): 1 skip epilogue math, 2 skip query TMA
   unsigned long long* stats;   // optional [kScoreStats] role-level stall cycles, summed over CTAs (may be null)
 };

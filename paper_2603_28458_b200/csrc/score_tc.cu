@@ -18,8 +18,8 @@
 //     SELECTED that key block — the refinement is run block-major ("inverted"), because a key tile that is
 //     loaded once and multiplied with N=256 query columns needs half the L2->SM bytes per scored pair of a
 //     query-major gather (16 KB of q vs 32 KB of keys per pair) and keeps the full N=256 MMA shape.
-//   * persistent CTAs (one per SM) pull items from a global cursor; a scheduler warp prefetches items so
-//     the global atomic + item load are off the TMA producer's critical path.
+//   * persistent CTAs (one per SM) pull items from a global cursor; the fetch of the next items is issued while the
+//     current one is produced, so the global atomic + item load are off the TMA producers' critical path.
 //   * multi-term products: operands may be split into bf16 segments (pooled keys: hi|lo; fp32 inputs:
 //     exact 3-way split); TERMS lists which A segments multiply each B segment, all accumulated into the
 //     same TMEM tile before the ReLU. Segment structure is a template parameter so the issue loop is
@@ -28,10 +28,10 @@
 //     the issuing thread keeps up, so the issue loop is written to be lean: warp-uniform control flow (all
 //     lanes wait, one elected lane issues), descriptors built by adding constants to per-stage bases.
 //
-// Warp roles (608 threads): warps 0-15 epilogue in two sets of eight (set = warp / 8 takes the groups with
+// Warp roles (640 threads): warps 0-15 epilogue in two sets of eight (set = warp / 8 takes the groups with
 // g % 2 == set, i.e. it owns one of the two TMEM accumulators; inside a set warp % 4 = TMEM lane quarter and
-// (warp / 4) % 2 = which PAIR of the group's 4 queries), warp 16 TMA producer, warp 17 MMA issuer + TMEM owner,
-// warp 18 scheduler. With the sets half a period apart each SM sub-partition always has warps of both sets to issue
+// (warp / 4) % 2 = which PAIR of the group's 4 queries), warps 16-18 TMA producers (chunks dealt round-robin; producer 0
+// also pulls work items from the global cursor), warp 19 MMA issuer + TMEM owner. With the sets half a period apart each SM sub-partition always has warps of both sets to issue
 // from (tcgen05.ld / LDS / shuffle latencies of one set hide under the FMNMX/FFMA2 stream of the other), and every
 // warp additionally keeps one 16-register tcgen05.ld in flight under its own math.
 #include "kernels.cuh"
@@ -43,10 +43,10 @@ namespace {
 
 constexpr int kEpiWarps = 16;
 constexpr int kEpiSetWarps = 8;  // epilogue warps per accumulator
-constexpr int kProducerWarp = 16;
-constexpr int kMmaWarp = 17;
-constexpr int kSchedWarp = 18;
-constexpr int kTcThreads = 19 * 32;
+constexpr int kProducerWarp = 16;  // first of kProducers TMA producer warps
+constexpr int kMaxProducers = 3;   // warps reserved for producers; a variant uses NPROD <= 3 of them
+constexpr int kMmaWarp = kProducerWarp + kMaxProducers;
+constexpr int kTcThreads = (kMmaWarp + 1) * 32;  // 640: one more warp would drop the register budget from 96 to 80
 constexpr int kMetaSlots = 8;
 constexpr int kUnitSlots = 4;
 constexpr uint32_t kAHalfBytes = kTileRows * 128;      // one 64-element K-half of one A segment: 16 KB
@@ -139,6 +139,9 @@ struct RowSum {
 template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8, bool STATS>
 __global__ void __launch_bounds__(kTcThreads, 1)
 score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, ScoreArgs a) {
+  // producer warps: three keep up with two 32 KB chunks per group (bf16); with one chunk per group (fp8) two are
+  // enough and a third only takes issue slots from the epilogue warps of its sub-partition while it polls
+  const uint32_t kProducers = a.producers;  // 1..kMaxProducers, chosen by the host per variant (HISA_TC_PRODUCERS overrides)
   constexpr int KH = FP8 ? 1 : 2;                     // 128-byte K slabs per operand segment
   constexpr int KBOX = FP8 ? 128 : 64;                // elements per slab
   constexpr uint32_t kASegBytes = KH * kAHalfBytes;   // one A segment: 16 KB (fp8) / 32 KB (bf16)
@@ -178,7 +181,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     for (int i = 0; i < NST; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
     for (int i = 0; i < ABUF; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&t_full[i], 1); mbar_init(&t_empty[i], kEpiSetWarps); }
-    for (int i = 0; i < kUnitSlots; ++i) { mbar_init(&u_full[i], 1); mbar_init(&u_empty[i], 1); }
+    for (int i = 0; i < kUnitSlots; ++i) { mbar_init(&u_full[i], 1); mbar_init(&u_empty[i], kProducers); }
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -196,39 +199,64 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   const uint32_t tmem_base = *s_tmem;
   const uint32_t meta_base = smem_u32(s_meta);
 
-  if (warp == kSchedWarp) {
-    // ================= scheduler: prefetch work items into the unit ring =================
-    if (lane == 0) {
-      const uint32_t nitems = *a.work_count;
-      for (uint32_t useq = 0;; ++useq) {
-        const uint32_t slot = useq % kUnitSlots;
-        mbar_wait(&u_empty[slot], ((useq / kUnitSlots) & 1u) ^ 1u);
-        const uint32_t id = atomicAdd(a.work_cursor, 1u);
-        WorkItem w;
-        if (id < nitems) {
-          w = a.work[id];
-        } else {
-          w.tile = 0; w.first = 0; w.count = 0; w.reserved = 0;
-        }
-        s_unit[slot] = w;
-        mbar_arrive(&u_full[slot]);
-        if (w.count == 0) break;
+  if (warp >= kProducerWarp && warp < kProducerWarp + kProducers) {
+    // ================= TMA producers (warp-uniform loops, one elected lane issues) =================
+    // Issuing the copies of a group (4 query boxes per chunk + 4 gate rows) from ONE thread costs more cycles than
+    // the tensor pipe needs for the group (measured: the lone producer was busy ~90 % of the time while the MMA
+    // warp waited for data). All producer warps walk the same item / group / chunk sequence and chunk c is issued by
+    // producer c % kProducers; whoever issues the first chunk of a group also writes its meta slot and gates.
+    // Producer 0 alone loads the operand tiles and passes the terminate marker on. Its lane 0 is also the work
+    // scheduler: items come from a global cursor (dynamic load balance over the persistent CTAs) and are published
+    // to all producers through the unit ring; the atomic and the item load of item i+2 / i+1 are issued while item i
+    // is being produced, so their latency never sits on the producer's critical path.
+    const uint32_t pid = warp - kProducerWarp;
+    uint32_t turn = 0;  // chunk counter modulo kProducers
+    uint32_t pub = 0, fid = 0, nitems = 0;
+    WorkItem fw;
+    fw.tile = fw.first = fw.count = fw.reserved = 0;
+    bool pub_done = false;
+    auto fetch_item = [&](uint32_t id) {
+      WorkItem w;
+      if (id < nitems) w = a.work[id];
+      else w.tile = w.first = w.count = w.reserved = 0;  // terminate marker
+      return w;
+    };
+    auto publish = [&](const WorkItem& w) {
+      const uint32_t slot = pub % kUnitSlots;
+      mbar_wait(&u_empty[slot], ((pub / kUnitSlots) & 1u) ^ 1u);
+      s_unit[slot] = w;
+      mbar_arrive(&u_full[slot]);
+      ++pub;
+      if (w.count == 0) pub_done = true;
+    };
+    if (pid == 0 && lane == 0) {
+      nitems = *a.work_count;
+      publish(fetch_item(atomicAdd(a.work_cursor, 1u)));
+      if (!pub_done) {
+        fw = fetch_item(atomicAdd(a.work_cursor, 1u));
+        fid = atomicAdd(a.work_cursor, 1u);
       }
     }
-  } else if (warp == kProducerWarp) {
-    // ================= TMA producer (warp-uniform loop, one elected lane issues) =================
     uint32_t stage = 0, sph = 1;  // chunk ring position and the parity to wait for on b_empty
     uint32_t ws = 0;              // meta / gate slot = group index % 8
     uint64_t st_unit = 0, st_a = 0, st_b = 0;
     const uint32_t a_smem = smem_u32(s_a), b_smem = smem_u32(s_b), w_smem = smem_u32(s_w);
     for (uint32_t useq = 0;; ++useq) {
+      if (pid == 0 && lane == 0 && !pub_done) {  // publish item useq + 1, start fetching useq + 2 and the id after it
+        publish(fw);
+        if (!pub_done) {
+          fw = fetch_item(fid);
+          fid = atomicAdd(a.work_cursor, 1u);
+        }
+      }
+      __syncwarp();
       const uint32_t slot = useq % kUnitSlots;
       wait_timed(&u_full[slot], (useq / kUnitSlots) & 1u, st_unit);
       const WorkItem item = s_unit[slot];
       __syncwarp();
       if (lane == 0) mbar_arrive(&u_empty[slot]);
       if (item.count == 0) {
-        if (lane == 0) {
+        if (lane == 0 && pid == 0) {
           mbar_wait(&b_empty[stage], sph);
           // both epilogue sets must see the marker: the set of group g reads slot ws, the other one slot ws + 1
           sts_u32(meta_base + ws * uint32_t(sizeof(GroupMeta)) + 32, kFlagTerminate << 8);
@@ -246,9 +274,9 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const uint32_t row0 = tile_row0(a, item.tile);
       const uint32_t valid_rows = tile_valid_rows(a, item.tile);
       const uint32_t col_add = a.list_mode ? (item.tile % a.segs_per_block) * kTileRows : item.tile * kTileRows;
-      wait_timed(&a_empty[a_buf], ((useq / ABUF) & 1u) ^ 1u, st_a);
+      if (pid == 0) wait_timed(&a_empty[a_buf], ((useq / ABUF) & 1u) ^ 1u, st_a);
       __syncwarp();
-      if (elect_one()) {
+      if (pid == 0 && elect_one()) {
         mbar_arrive_expect_tx(&a_full[a_buf], NSEG_A * kASegBytes);
 #pragma unroll
         for (int ia = 0; ia < NSEG_A; ++ia)
@@ -284,9 +312,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           const uint32_t gg = gb + gi;
           const uint32_t nvalid = min(uint32_t(kGroupQ), item.count - gg * kGroupQ);
           const uint32_t flags = (gg == 0 ? kFlagFirst : 0u) | (gg + 1 == ngroups ? kFlagLast : 0u);
-          wait_timed(&b_empty[stage], sph, st_b);  // first chunk of the group: also guards the meta/gate slot
+          const bool mine0 = turn == pid;  // this producer issues the group's first chunk (and its meta + gates)
+          if (mine0) wait_timed(&b_empty[stage], sph, st_b);  // also guards the meta/gate slot
           __syncwarp();
-          if (elect_one()) {
+          if (mine0 && elect_one()) {
             const uint32_t maddr = meta_base + ws * uint32_t(sizeof(GroupMeta));
             sts_v4(maddr, qrow[0], qrow[1], qrow[2], qrow[3]);
             sts_v4(maddr + 16, qcol[0], qcol[1], qcol[2], qcol[3]);
@@ -306,11 +335,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           for (int ib = 0; ib < NSEG_B; ++ib)
 #pragma unroll
             for (int kh = 0; kh < KH; ++kh) {
-              if (ib + kh > 0) {
-                wait_timed(&b_empty[stage], sph, st_b);
-                __syncwarp();
-              }
-              if (elect_one()) {
+              const bool mine = turn == pid;
+              if (mine && ib + kh > 0) wait_timed(&b_empty[stage], sph, st_b);
+              __syncwarp();
+              if (mine && elect_one()) {
                 const uint32_t fbar = smem_u32(&b_full[stage]);
                 const uint32_t gate_bytes = (ib + kh == 0 && !(a.debug_flags & 4u)) ? nvalid * kGateRowBytes : 0u;
                 if (a.debug_flags & 2u) {
@@ -327,6 +355,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
               }
               __syncwarp();
               if (++stage == NST) { stage = 0; sph ^= 1u; }
+              if (++turn == kProducers) turn = 0;
             }
           ws = (ws + 1) % kMetaSlots;
         }
@@ -465,6 +494,11 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         reduce_frag(vx, gw[0], gw[1], a2, a3);
         tmem_ld_wait();
         if (act1) tmem_ld_16x128b_x8(t_lane + kHeads, vx);             // F(1, 0, 0)
+        if (a.debug_flags & 8u) {  // timing experiment only: hand the accumulator back half way (results are garbage)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_addr(t_empty_addr);
+        }
         reduce_frag(vy, gw[2], gw[3], a2, a3);
         f.step1(a0, a1, a2, a3, b0);
         float* dst0 = a.out + uint64_t(qrows.x) * a.out_stride + qcols.x + row;
@@ -491,7 +525,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         // all dots of the group are in registers: hand the accumulator back to the MMA warp
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_addr(t_empty_addr);
+        if (lane == 0 && !(a.debug_flags & 8u)) mbar_arrive_addr(t_empty_addr);
         if (act1) {
           reduce_frag(vy, gw[2], gw[3], a2, a3);
           f.step1(a0, a1, a2, a3, b0);
