@@ -81,12 +81,6 @@ struct SmemLayout {
   static constexpr uint32_t total = tmem_off + 16;
 };
 
-__device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
-__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t a) {
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(a) : "memory");
-}
 // packed fp32x2 FMA (sm_100): acc.{x,y} += a.{x,y} * b.{x,y}
 __device__ __forceinline__ void ffma2(float2& acc, float a0, float a1, float b0, float b1) {
   uint64_t av, bv, cv;

@@ -763,6 +763,25 @@ __device__ __forceinline__ uint32_t score_key_fast(float f) {
   return b ^ (uint32_t(int32_t(b) >> 31) | 0x80000000u);
 }
 
+// hist[(d >> shift)] += 1 when d <= span, as ONE predicated RED on a 32-bit shared address (the generic-pointer
+// atomicAdd cost ten instructions per key: a branch pair and a re-derived shared window base around every ATOMS)
+__device__ __forceinline__ void hist_inc_if_le(uint32_t hist_addr, uint32_t d, uint32_t span, uint32_t shift) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
+      "setp.le.u32 p, %1, %2;\n\t"
+      "shr.u32 t, %1, %3;\n\t"
+      "shl.b32 t, t, 2;\n\t"
+      "add.u32 t, t, %0;\n\t"
+      "@p red.shared.add.u32 [t], 1;\n\t}"
+      ::"r"(hist_addr), "r"(d), "r"(span), "r"(shift)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t atom_shared_inc(uint32_t addr) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(addr) : "memory");
+  return old;
+}
+
 template <int THREADS, int PER4>
 __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
   constexpr int KPT = PER4 * 4;
@@ -778,6 +797,7 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
   uint32_t* ssel = list + THREADS;          // [sel_stride]
   uint32_t* scratch = ssel + a.sel_stride;  // [96]
   __shared__ __align__(8) uint64_t bar;
+  const uint32_t hist_addr = smem_u32(hist), list_addr = smem_u32(list), fill_addr = smem_u32(scratch + 2);
 
   const uint32_t row = blockIdx.x;
   const uint32_t tid = threadIdx.x;
@@ -891,9 +911,19 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
     const uint32_t span = hi - lo;
     if (in_range <= uint32_t(THREADS)) {
       // compact the keys of the threshold range (order is irrelevant) and rank them all-pairs
+      {
+        uint32_t h0 = 0, h1 = 0;  // bit e <=> key e lies in the threshold range (few threads have any)
 #pragma unroll
-      for (int e = 0; e < KPT; ++e)
-        if (k[e] - lo <= span) list[atomicAdd(&scratch[2], 1u)] = k[e];
+        for (int e = 0; e < KPT; ++e) {
+          const uint32_t hit = (k[e] - lo <= span) ? 1u : 0u;
+          if (e < 32) h0 |= hit << e; else h1 |= hit << (e - 32);
+        }
+        if (h0 | h1) {
+#pragma unroll
+          for (int e = 0; e < KPT; ++e)
+            if ((e < 32 ? h0 >> e : h1 >> (e - 32)) & 1u) sts_u32(list_addr + atom_shared_inc(fill_addr) * 4u, k[e]);
+        }
+      }
       __syncthreads();
       if (tid < in_range) {
         const uint32_t mine = list[tid];
@@ -918,10 +948,7 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
     const uint32_t nb = 32 - __clz(span);
     const uint32_t shift = nb > kBinBits ? nb - kBinBits : 0u;
 #pragma unroll
-    for (int e = 0; e < KPT; ++e) {
-      const uint32_t dlt = k[e] - lo;  // zero keys wrap around to a huge value (lo > 0)
-      if (dlt <= span) atomicAdd(&hist[dlt >> shift], 1u);
-    }
+    for (int e = 0; e < KPT; ++e) hist_inc_if_le(hist_addr, k[e] - lo, span, shift);  // zero keys wrap to a huge value
     __syncthreads();
     uint32_t hb[BPT];
     uint32_t loc = 0;
@@ -1016,23 +1043,39 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
     delta0 = slot0 < ns ? int32_t((ssel[slot0] - slot0) << bshift) : 0;
     delta1 = slot0 + 1 < ns ? int32_t((ssel[slot0 + 1] - (slot0 + 1)) << bshift) : 0;
   }
-  auto emit = [&](uint32_t idx) {
-    int32_t v;
-    if (two_block) v = int32_t(idx) + (idx < boundary ? delta0 : delta1);
-    else v = position_of(idx);
-    if (staged) hist[o] = uint32_t(v);
-    else orow[o] = v;
-    ++o;
-  };
-  while (m0) {
-    const uint32_t e = __ffs(m0) - 1;
-    m0 &= m0 - 1;
-    emit(first + e);
-  }
-  while (m1) {
-    const uint32_t e = __ffs(m1) - 1;
-    m1 &= m1 - 1;
-    emit(first + 32 + e);
+  if (staged && (two_block || !cand)) {
+    // common case, branch-free body: position = idx + per-thread delta, staged through shared memory
+    if (!cand) boundary = 0xFFFFFFFFu;  // identity mapping: delta0 = delta1 = 0
+    uint32_t oaddr = hist_addr + o * 4u;
+    while (m0) {
+      const uint32_t idx = first + __ffs(m0) - 1;
+      m0 &= m0 - 1;
+      sts_u32(oaddr, idx + uint32_t(idx < boundary ? delta0 : delta1));
+      oaddr += 4;
+    }
+    while (m1) {
+      const uint32_t idx = first + 31 + __ffs(m1);
+      m1 &= m1 - 1;
+      sts_u32(oaddr, idx + uint32_t(idx < boundary ? delta0 : delta1));
+      oaddr += 4;
+    }
+  } else {
+    auto emit = [&](uint32_t idx) {
+      const int32_t v = position_of(idx);
+      if (staged) hist[o] = uint32_t(v);
+      else orow[o] = v;
+      ++o;
+    };
+    while (m0) {
+      const uint32_t e = __ffs(m0) - 1;
+      m0 &= m0 - 1;
+      emit(first + e);
+    }
+    while (m1) {
+      const uint32_t e = __ffs(m1) - 1;
+      m1 &= m1 - 1;
+      emit(first + 32 + e);
+    }
   }
   if (tid == 0 && a.out_count) a.out_count[row] = count;
   if (staged) {
