@@ -285,7 +285,7 @@ def run_b200(a, rank, world, local_rank):
     k_ms = stages["score_tokens_ms"] / max(stages["calls"], 1)
     achieved = flops_s2 / (k_ms * 1e-3) / 1e12 if k_ms > 0 else 0.0
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic_score_tc_stage2.json")
+    tpath = os.path.join(ROOT, "profiles", "traffic_score_tc_stage2_fp8.json" if a.dtype == "fp8" else "traffic_score_tc_stage2.json")
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
@@ -305,12 +305,16 @@ def run_b200(a, rank, world, local_rank):
     for st_name, st in st_stages["stalls"].items():
         cta = max(st["cta"], 1)
         stalls[st_name] = {kk: (round(vv / cta, 4) if kk != "groups" else vv) for kk, vv in st.items()
-                           if kk != "cta" and not kk.startswith("epi_")}
+                           if kk not in ("cta", "cta_max") and not kk.startswith("epi_")}
         # SM clock the kernel really ran at: CTA lifetime cycles (one persistent CTA per SM) / its CUDA-event time
         st_ms = st_stages["score_blocks_ms" if st_name == "stage1" else "score_tokens_ms"]
         if st_ms > 0:
             n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-            stalls[st_name]["sm_mhz_in_kernel"] = round(st["cta"] / n_sm / (st_ms * 1e-3) / 1e6, 1)
+            calls_st = max(st_stages["calls"], 1)
+            # mean CTA lifetime / longest CTA lifetime: 1.0 = perfectly balanced persistent CTAs
+            stalls[st_name]["cta_balance"] = round(st["cta"] / n_sm / calls_st / max(st["cta_max"], 1), 4)
+            # SM clock the kernel really ran at: longest CTA lifetime (cycles) / the kernel's CUDA-event time
+            stalls[st_name]["sm_mhz_in_kernel"] = round(st["cta_max"] / (st_ms / calls_st * 1e-3) / 1e6, 1)
 
     # ---- in-run comparison: the flat DSA indexer built from the same kernels
     flat = None

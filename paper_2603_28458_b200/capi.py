@@ -238,7 +238,7 @@ class Indexer:
         return st.as_dict()
 
     STALL_NAMES = ["cta", "prod_wait_sched", "prod_wait_tilebuf", "prod_wait_qstage", "mma_wait_qdata", "mma_wait_tile",
-                   "mma_wait_epilogue", "mma_wait_gates", "epi_wait_mma", "epi_busy", "groups"]
+                   "mma_wait_epilogue", "mma_wait_gates", "cta_max", "epi_busy", "groups"]
 
     def scorer_stall_cycles(self) -> dict:
         a, b = (C.c_uint64 * 16)(), (C.c_uint64 * 16)()

@@ -68,7 +68,7 @@ enum ScoreStat : int {
   kStatMmaAFull,         // MMA issuer waiting for tile data
   kStatMmaTEmpty,        // MMA issuer waiting for the epilogue to drain an accumulator
   kStatEpiWFull,         // MMA issuer waiting for the gates of a group (they ride with its first query chunk)
-  kStatEpiTFull,         // epilogue (warp 0) waiting for the MMA
+  kStatCtaMax,           // longest CTA lifetime (max, not a sum)
   kStatEpiBusy,          // epilogue (warp 0) cycles between t_full and t_empty arrive
   kStatGroups,           // groups processed
   kScoreStats

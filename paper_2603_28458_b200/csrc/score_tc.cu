@@ -541,7 +541,11 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
   }
-  if (STATS && a.stats && threadIdx.x == 0) atomicAdd(a.stats + kStatCta, (unsigned long long)(clock64() - cta_c0));
+  if (STATS && a.stats && threadIdx.x == 0) {
+    const unsigned long long life = (unsigned long long)(clock64() - cta_c0);
+    atomicAdd(a.stats + kStatCta, life);
+    atomicMax(a.stats + kStatCtaMax, life);  // longest-lived CTA of any launch since the last read: tail imbalance
+  }
 }
 
 template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8, bool STATS>
