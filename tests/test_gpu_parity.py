@@ -479,3 +479,79 @@ def test_fp8_rejects_unsupported_shapes():
     with pytest.raises(capi.HisaError) as e:
         capi.Indexer(capi.make_config(128, 4, 64, 64, 128, capi.DTYPE_FP8, scorer=capi.SCORER_SIMT))
     assert e.value.name == "Unsupported"
+
+
+# ------------------------------------------------------------------------------------------ full-size configurations
+def _numpy_problem(oracle, L, rows, seed, B, m, k, H=64, d=128):
+    """bf16-rounded random inputs for `rows` query positions against L keys (numpy generator: the C++ hisa-rng-v1
+    generator is too slow for gigabytes; both the oracle and the GPU get the same arrays)."""
+    rng = np.random.default_rng(seed)
+    keys = rng.standard_normal((L, d), dtype=np.float32)
+    q = rng.standard_normal((len(rows), H, d), dtype=np.float32)
+    w = rng.uniform(0.5, 1.5, (len(rows), H)).astype(np.float32)
+    prob = oracle.Problem(q, w, keys, np.asarray(rows, np.uint32), block_size=B, block_budget=m, token_budget=k)
+    qb, kb = round_problem_to_bf16(prob)
+    return prob, qb, kb
+
+
+def test_headline_config_c3_properties_and_sampled_rows(oracle):
+    """BASELINE config[2] (L=65536, H=64, d=128, B=128, m=64, k=2048, bf16): every row of the regime-equivalence
+    prefix t + 1 <= mB plus a stratified sample up to t = L - 1. Size-independent properties on all rows
+    (hisa/audit.hpp:37-49), the CPU oracle on a sample of them."""
+    L, B, m, k = 65536, 128, 64, 2048
+    lim = m * B
+    rng = np.random.default_rng(5)
+    tail = np.unique(np.concatenate([[lim, lim + 1, (m + 2) * B - 1, (m + 2) * B, L - B - 1, L - B, L - 2, L - 1],
+                                     rng.integers(lim, L, 2040)]))
+    rows = np.concatenate([np.arange(lim), tail]).astype(np.uint32)
+    prob, qb, kb = _numpy_problem(oracle, L, rows, 31, B, m, k)
+    Q = len(rows)
+    with indexer_for(prob) as ix:
+        ix.upload_keys(kb)
+        h = ix.hisa_select(qb, prob.gates, rows)
+        f = ix.dsa_select(qb[:lim], prob.gates[:lim], rows[:lim])
+    # regime equivalence: t + 1 <= mB  =>  hisa == dsa exactly
+    assert np.array_equal(h["idx"][:lim], f["idx"]) and np.array_equal(h["count"][:lim], f["count"])
+    # dense regime, subset chain, cardinality, ordering, forced blocks
+    for t in (0, 1, 777, k - 1):
+        assert h["idx"][t, :t + 1].tolist() == list(range(t + 1)) and h["count"][t] == t + 1
+    valid = h["idx"] >= 0
+    t_col = rows[:, None].astype(np.int64)
+    assert (h["count"] == np.minimum(k, h["cand"])).all() and (valid.sum(1) == h["count"]).all()
+    assert ((h["idx"] <= t_col) | ~valid).all()
+    assert (np.diff(np.where(valid, h["idx"], np.iinfo(np.int32).max).astype(np.int64), axis=1) >= 0).all()
+    assert (h["nblocks"] <= m + 2).all() and (h["blocks"][:, 0] == 0).all()
+    assert (h["blocks"][np.arange(Q), h["nblocks"] - 1] == rows // B).all()
+    late = rows >= (m + 2) * B
+    assert (h["nblocks"][late] >= m).all() and (h["cand"][late] <= (m + 2) * B).all()
+    blk_of = np.where(valid, h["idx"] // B, -1)
+    for r in range(0, Q, 301):
+        assert set(blk_of[r][valid[r]].tolist()) <= set(h["blocks"][r, :h["nblocks"][r]].tolist())
+    # oracle on a sample: edges of the regimes + random rows of the sparse regime
+    sample = np.unique(np.concatenate([[0, k - 1, k, lim - 1], lim + np.arange(0, len(tail), 85)]))
+    ex, near, rec = compare_selection(oracle, prob, "hisa", h, sample, BF16_RTOL)
+    print(f"C3 sample of {len(sample)} rows: exact={ex} near-tie={near} recall={rec:.6f}")
+    assert rec >= 0.999
+
+
+def test_decode_config_c5_128k_incremental_append(oracle):
+    """BASELINE config[4] at L=131072: 64 queries at the newest position; the last tokens arrive one at a time through
+    the incremental tail-block update before each selection (BlockSummaryCache::append, block_summary.hpp:27-30)."""
+    L, B, m, k, steps = 131072, 128, 64, 2048, 5
+    rows = np.full(64, L - 1, np.uint32)
+    prob, qb, kb = _numpy_problem(oracle, L, rows, 77, B, m, k)
+    with indexer_for(prob) as ix:
+        ix.upload_keys(kb[:L - steps])
+        ix.pool_build()
+        for s in range(steps):                       # decode loop: append one key, select for the new position
+            at = L - steps + s
+            ix.pool_append(kb[at:at + 1])
+            pos = np.full(64, at, np.uint32)
+            h = ix.hisa_select(qb, prob.gates, pos)
+            assert (h["count"] == k).all() and (h["blocks"][np.arange(64), h["nblocks"] - 1] == at // B).all()
+        sums, counts, pooled = ix.pool_read()
+    osums, ocounts, opooled = oracle.pool_build(prob.keys, B)
+    assert counts.tolist() == ocounts.tolist() and np.array_equal(sums, osums) and np.array_equal(pooled, opooled)
+    ex, near, rec = compare_selection(oracle, prob, "hisa", h, np.arange(64), BF16_RTOL)
+    print(f"C5 decode 128K: exact={ex} near-tie={near} recall={rec:.6f}")
+    assert rec >= 0.999
