@@ -46,6 +46,7 @@ constexpr int kEpiSetWarps = 8;  // epilogue warps per accumulator
 constexpr int kProducerWarp = 16;  // first of kProducers TMA producer warps
 constexpr int kMaxProducers = 3;   // warps reserved for producers; a variant uses NPROD <= 3 of them
 constexpr int kMmaWarp = kProducerWarp + kMaxProducers;
+constexpr int kEpiRegs = 104, kOtherRegs = 64;
 constexpr int kTcThreads = (kMmaWarp + 1) * 32;  // 640: one more warp would drop the register budget from 96 to 80
 constexpr int kMetaSlots = 8;
 constexpr int kUnitSlots = 4;
@@ -193,6 +194,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   const uint32_t tmem_base = *s_tmem;
   const uint32_t meta_base = smem_u32(s_meta);
 
+  // Register re-partitioning: the four non-epilogue warps (one warp group) give up a third of their registers, which
+  // is exactly what lifts the sixteen epilogue warps from the 96-register launch budget to 104
+  // (512 * 104 + 128 * 64 = 640 * 96). One textual setmaxnreg per warp group, as the instruction requires.
+  if (warp >= kEpiWarps) setmaxnreg_dec<kOtherRegs>();
   if (warp >= kProducerWarp && warp < kProducerWarp + kProducers) {
     // ================= TMA producers (warp-uniform loops, one elected lane issues) =================
     // Issuing the copies of a group (4 query boxes per chunk + 4 gate rows) from ONE thread costs more cycles than
@@ -444,6 +449,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     // two key rows per row half, so it needs only 16 gates (64 B) per query instead of all 64: the gate traffic
     // through the 128 B/clk shared-memory return path is what bounded a one-row-per-thread (32x32b) epilogue. The 4
     // lanes sharing a row are summed by shuffles.
+    setmaxnreg_inc<kEpiRegs>();
     const uint32_t set = warp >> 3;        // accumulator / group parity this warp serves
     const uint32_t quarter = warp & 3u;
     const uint32_t qp = ((warp >> 2) & 1u) * 2u;  // first of the two queries this warp reduces
