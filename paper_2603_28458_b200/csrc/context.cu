@@ -355,6 +355,7 @@ int run_scorer(hisa_cuda_ctx* ctx, const ScoreJob& j) {
   a.fp8 = j.a8 ? 1u : 0u;
   a.a_scale = j.a_scale;
   a.debug_flags = env_u32("HISA_TC_DEBUG", 0);
+  a.epi_sleep_ns = env_u32("HISA_TC_EPI_SLEEP", 0);
   a.producers = std::min<uint32_t>(std::max<uint32_t>(env_u32("HISA_TC_PRODUCERS", j.a8 ? 2 : 3), 1), 3);
   a.stats = nullptr;
   if (ctx->profiling && ctx->stall_stats) {
@@ -404,16 +405,26 @@ int ensure_pool(hisa_cuda_ctx* ctx) {
   return hisa_cuda_pool_build(ctx);
 }
 
+// Queries per dense work item. The configured chunk amortises a tile load over many queries; calls with few rows
+// (decode batches, the paper's 1024-row tail) would then produce fewer items than there are SMs, so the chunk is
+// halved until every SM has about two items (never below two MMA groups).
+uint32_t dense_chunk_for(const hisa_cuda_ctx* ctx, uint64_t nq, uint32_t ntiles) {
+  uint32_t chunk = ctx->chunk_dense;
+  while (chunk > 8 && ((nq + chunk - 1) / chunk) * ntiles < 2ull * uint64_t(ctx->num_sms)) chunk /= 2;
+  return chunk;
+}
+
 // stage 1: J[q, b] for rows [0, nq) -> ctx->J with stride Mpad
 int run_score_blocks(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, uint64_t nq, uint32_t Mpad) {
   const uint32_t M = uint32_t(num_blocks_of(ctx));
   const uint32_t ntiles = Mpad / kTileRows;
-  const uint32_t nchunks = uint32_t((nq + ctx->chunk_dense - 1) / ctx->chunk_dense);
+  const uint32_t chunk = dense_chunk_for(ctx, nq, ntiles);
+  const uint32_t nchunks = uint32_t((nq + chunk - 1) / chunk);
   HISA_TRY(ensure(ctx, ctx->work, size_t(nchunks) * ntiles * sizeof(WorkItem)));
   HISA_TRY(ensure(ctx, ctx->J, size_t(nq) * Mpad * sizeof(float)));
   uint32_t* sc = ctx->scalars.as<uint32_t>();
   StageTimer timer(ctx, kStScoreBlocks);
-  count_launches(ctx, launch_build_dense_work(p.pos + q0, uint32_t(nq), ctx->chunk_dense, uint32_t(ctx->seq_len),
+  count_launches(ctx, launch_build_dense_work(p.pos + q0, uint32_t(nq), chunk, uint32_t(ctx->seq_len),
                                               ctx->cfg.block_size, ntiles, ctx->work.as<WorkItem>(), sc, sc + 1,
                                               ctx->stream));
   ScoreJob j{};
@@ -536,13 +547,14 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
     if (strat == kDsa) {
       // ---- flat indexer: score the whole causal prefix, then top-k (dsa.hpp:29-32) ----
       const uint32_t ntiles = Lpad / kTileRows;
-      const uint32_t nchunks = uint32_t((nq + ctx->chunk_dense - 1) / ctx->chunk_dense);
+      const uint32_t chunk = dense_chunk_for(ctx, nq, ntiles);
+      const uint32_t nchunks = uint32_t((nq + chunk - 1) / chunk);
       HISA_TRY(ensure(ctx, ctx->work, size_t(nchunks) * ntiles * sizeof(WorkItem)));
       HISA_TRY(ensure(ctx, ctx->flat, size_t(nq) * Lpad * 4));
       uint32_t* sc = ctx->scalars.as<uint32_t>();
       {
         StageTimer timer(ctx, kStScoreTokens);
-        count_launches(ctx, launch_build_dense_work(p.pos + q0, uint32_t(nq), ctx->chunk_dense, L, 1, ntiles,
+        count_launches(ctx, launch_build_dense_work(p.pos + q0, uint32_t(nq), chunk, L, 1, ntiles,
                                                     ctx->work.as<WorkItem>(), sc, sc + 1, ctx->stream));
         ScoreJob j{};
         j.stats_slot = 1;
@@ -1291,13 +1303,14 @@ int hisa_cuda_score_tokens(hisa_cuda_ctx* ctx, const void* queries, const float*
   if (Q > uint64_t(ctx->chunk_dense) * 4096) return fail(ctx, HISA_ERR_UNSUPPORTED, "score_tokens: too many rows in one call");
   HISA_TRY(ensure(ctx, ctx->scalars, 64));
   const uint32_t ntiles = Lpad / kTileRows;
-  const uint32_t nchunks = uint32_t((Q + ctx->chunk_dense - 1) / ctx->chunk_dense);
+  const uint32_t chunk = dense_chunk_for(ctx, Q, ntiles);
+  const uint32_t nchunks = uint32_t((Q + chunk - 1) / chunk);
   HISA_TRY(ensure(ctx, ctx->work, size_t(nchunks) * ntiles * sizeof(WorkItem)));
   const bool out_dev = is_device_ptr(out_scores);
   if (!out_dev) HISA_TRY(ensure(ctx, ctx->flat, size_t(Q) * Lpad * 4));
   uint32_t* sc = ctx->scalars.as<uint32_t>();
   StageTimer* timer = new StageTimer(ctx, kStScoreTokens);
-  count_launches(ctx, launch_build_dense_work(p.pos, uint32_t(Q), ctx->chunk_dense, L, 1, ntiles, ctx->work.as<WorkItem>(),
+  count_launches(ctx, launch_build_dense_work(p.pos, uint32_t(Q), chunk, L, 1, ntiles, ctx->work.as<WorkItem>(),
                                               sc, sc + 1, ctx->stream));
   ScoreJob j{};
   set_token_operands(ctx, p, 0, j);

@@ -54,6 +54,7 @@ struct ScoreArgs {
   uint32_t fp8;                // operands are e4m3 bytes [rows, 128] (kind::f8f6f4); nseg_a = nseg_b = 1
   const float* a_scale;        // fp8: per-row dequantisation scale of the A operand (may be null = 1)
   uint32_t producers;          // TMA producer warps that take part (1..3)
+  uint32_t epi_sleep_ns;       // nanosleep between polls of the epilogue warps' accumulator barrier (0 = spin)
   uint32_t debug_flags;        // timing experiments only (HISA_TC_DEBUG): 1 skip epilogue math, 2 skip query TMA
   unsigned long long* stats;   // optional [kScoreStats] role-level stall cycles, summed over CTAs (may be null)
 };

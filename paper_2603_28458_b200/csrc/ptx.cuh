@@ -96,6 +96,21 @@ __device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t parity) {
     }
   }
 }
+// same with a nanosleep between polls: warps that wait long (epilogue warps when the kernel is MMA- or feed-bound)
+// stop competing for issue slots and burning power while they poll
+__device__ __forceinline__ void mbar_wait_addr_sleep(uint32_t bar, uint32_t parity, uint32_t sleep_ns) {
+  if (mbar_try_wait_addr(bar, parity)) return;
+  const uint64_t t0 = global_timer_ns();
+  uint32_t spins = 0;
+  while (!mbar_try_wait_addr(bar, parity)) {
+    if (sleep_ns) __nanosleep(sleep_ns);
+    if ((++spins & 0xFFu) == 0 && global_timer_ns() - t0 > HISA_MBAR_TIMEOUT_NS) {
+      printf("hisa: mbarrier wait timed out (block %d thread %d bar 0x%x parity %u)\n", blockIdx.x, threadIdx.x, bar,
+             parity);
+      asm volatile("trap;");
+    }
+  }
+}
 __device__ __forceinline__ void mbar_arrive_addr(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }

@@ -461,7 +461,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     uint32_t vx[16], vy[16];
     for (uint32_t g = set;; g += 2) {
       const uint32_t ws = g % kMetaSlots;
-      mbar_wait_addr(t_full_addr, (g >> 1) & 1u);
+      mbar_wait_addr_sleep(t_full_addr, (g >> 1) & 1u, a.epi_sleep_ns);
       const uint32_t maddr = meta_base + ws * uint32_t(sizeof(GroupMeta));
       const uint32_t word = lds_u32(maddr + 32);
       if ((word >> 8) & kFlagTerminate) break;
