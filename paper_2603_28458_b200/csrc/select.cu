@@ -638,14 +638,14 @@ __global__ void __launch_bounds__(THREADS) select_cta_kernel(SelectArgs a) {
           j = jj - 1;
         }
       }
-      scratch[40] = tid * BPT + j;
-      scratch[41] = c;
-      scratch[42] = hb[j];
+      scratch[80] = tid * BPT + j;
+      scratch[81] = c;
+      scratch[82] = hb[j];
     }
     __syncthreads();
-    const uint32_t bin = scratch[40];
-    const uint32_t in_bin = scratch[42];
-    kk -= scratch[41];
+    const uint32_t bin = scratch[80];
+    const uint32_t in_bin = scratch[82];
+    kk -= scratch[81];
     lo = lo + (bin << shift);
     const uint32_t width = (shift == 0) ? 0u : ((1u << shift) - 1u);
     hi = min(hi, lo + width);
@@ -975,17 +975,17 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
           j = jj - 1;
         }
       }
-      scratch[40] = tid * BPT + j;
-      scratch[41] = c;
-      scratch[42] = hb[j];
+      scratch[80] = tid * BPT + j;
+      scratch[81] = c;
+      scratch[82] = hb[j];
     }
     // the histogram words this thread owns are dead now: clear them for the next level / keep them clean
 #pragma unroll
     for (int j = 0; j < BPT / 4; ++j) reinterpret_cast<uint4*>(hist)[tid * (BPT / 4) + j] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
-    const uint32_t bin = scratch[40];
-    in_range = scratch[42];
-    kk -= scratch[41];
+    const uint32_t bin = scratch[80];
+    in_range = scratch[82];
+    kk -= scratch[81];
     lo = lo + (bin << shift);
     const uint32_t width = (shift == 0) ? 0u : ((1u << shift) - 1u);
     hi = min(hi, lo + width);
