@@ -776,6 +776,14 @@ __device__ __forceinline__ void hist_inc_if_le(uint32_t hist_addr, uint32_t d, u
       ::"r"(hist_addr), "r"(d), "r"(span), "r"(shift)
       : "memory");
 }
+// mask |= bit when d <= span
+__device__ __forceinline__ void or_bit_if_le(uint32_t& mask, uint32_t d, uint32_t span, uint32_t bit) {
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.le.u32 p, %1, %2;\n\t"
+      "@p or.b32 %0, %0, %3;\n\t}"
+      : "+r"(mask)
+      : "r"(d), "r"(span), "r"(bit));
+}
 __device__ __forceinline__ uint32_t atom_shared_inc(uint32_t addr) {
   uint32_t old;
   asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(addr) : "memory");
@@ -914,9 +922,9 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
       {
         uint32_t h0 = 0, h1 = 0;  // bit e <=> key e lies in the threshold range (few threads have any)
 #pragma unroll
-        for (int e = 0; e < KPT; ++e) {
-          const uint32_t hit = (k[e] - lo <= span) ? 1u : 0u;
-          if (e < 32) h0 |= hit << e; else h1 |= hit << (e - 32);
+        for (int e = 0; e < KPT; ++e) {  // subtract, compare, predicated OR with an immediate
+          if (e < 32) or_bit_if_le(h0, k[e] - lo, span, 1u << e);
+          else or_bit_if_le(h1, k[e] - lo, span, 1u << (e - 32));
         }
         if (h0 | h1) {
 #pragma unroll
@@ -998,10 +1006,9 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
   uint32_t cE = 0;
   if (all_ties) {
 #pragma unroll
-    for (int e = 0; e < KPT; ++e) {
-      if (k[e] >= T) {
-        if (e < 32) m0 |= 1u << e; else m1 |= 1u << (e - 32);
-      }
+    for (int e = 0; e < KPT; ++e) {  // k >= T  <=>  k - T <= ~T as unsigned (k < T wraps above ~T)
+      if (e < 32) or_bit_if_le(m0, k[e] - T, ~T, 1u << e);
+      else or_bit_if_le(m1, k[e] - T, ~T, 1u << (e - 32));
     }
   } else {
 #pragma unroll
