@@ -271,6 +271,7 @@ def run_b200(a, rank, world, local_rank):
         ms_total, stages, launches = timed(step_hisa, a.steps, a.warmup, profile=True)
     ms_step = ms_total / a.steps
     value = Q * a.steps / (ms_total * 1e-3)
+    hisa_idx = out_idx.clone()  # the device-path result: the host-buffer (e2e) path must reproduce it bit for bit
 
     # ---- roofline of the dominant kernel (stage-2 fused scorer): algorithmic flops / live CUDA-event time
     cand_sum = int(out_cand.to(torch.int64).sum().item())
@@ -299,6 +300,28 @@ def run_b200(a, rank, world, local_rank):
                 "flops_per_launch": flops_s2, "kernel_ms": k_ms}
     per_call = {kk: (vv / max(stages["calls"], 1) if kk.endswith("_ms") else vv) for kk, vv in stages.items()
                 if kk != "stalls"}
+    # ---- every stage against the roofline that bounds it (algorithmic work / CUDA-event time)
+    pos64 = pos.to(torch.int64).clamp(max=L - 1)
+    elig_sum = int((pos64 // B + 1).sum().item())                       # Σ_t eligible blocks
+    nsel_max = nq * (m + 2)
+    eb = q.element_size()
+
+    def stage_roof(ms, bound, work, note, tensor_peak=None):
+        peak = (tensor_peak or peaks["tflops"]) if bound == "tensor" else peaks["hbm_gbs"]
+        ach = work / (ms * 1e-3) / (1e12 if bound == "tensor" else 1e9) if ms > 0 else 0.0
+        return {"bound": bound, "ms": round(ms, 4), "achieved": round(ach, 1), "peak": peak,
+                "unit": "TFLOP/s" if bound == "tensor" else "GB/s", "frac": round(ach / peak, 4), "work": note}
+    stage_rooflines = {
+        "score_blocks": stage_roof(per_call["score_blocks_ms"], "tensor", 2.0 * d * H * elig_sum,
+                                   "2*d*H*sum_t(eligible blocks); the kernel spends 2 bf16 MMA terms per dot (hi|lo pooled keys)",
+                                   tensor_peak=load_peaks()["tflops"]),
+        "select_blocks": stage_roof(per_call["select_blocks_ms"], "hbm", 4.0 * elig_sum + 4.0 * nsel_max,
+                                    "block scores read + block lists written (J is mostly L2-resident: 128 MiB)"),
+        "score_tokens": stage_roof(per_call["score_tokens_ms"], "tensor", flops_s2, "2*d*H*sum_t|Omega_t|"),
+        "top_k": stage_roof(per_call["top_k_ms"], "hbm", 4.0 * cand_sum + 4.0 * nq * k,
+                            "candidate scores read + [Q,k] int32 indices written"),
+    }
+    _ = eb
     # role-level stall accounting: a short separate pass with the instrumented scorer instantiation (not timed)
     _, st_stages, _ = timed(step_hisa, min(a.steps, 3), 0, profile=True, stall_stats=True)
     stalls = {}
@@ -353,7 +376,7 @@ def run_b200(a, rank, world, local_rank):
             t = torch.tensor([dt], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        same = bool(torch.equal(hidx.to(dev), out_idx)) if a.flat_steps == 0 else None
+        same = bool(torch.equal(hidx.to(dev), hisa_idx))
         e2e = {"value": Q * a.e2e_steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": int(hq.numel() * hq.element_size() + hw.numel() * 4 + hpos.numel() * 4) * world,
                "d2h_bytes_per_step": int(hidx.numel() * 4 + hcnt.numel() * 4) * world,
@@ -396,7 +419,8 @@ def run_b200(a, rank, world, local_rank):
                        "sharding": f"query tiles of {TILE_ROWS} rows round-robin over ranks; keys NCCL-broadcast; "
                                    "indices all-gathered inside the step" if world > 1 else "single GPU"},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
-            "roofline": roofline, "cpu_baseline": cpu, "flat_dsa": flat, "stages_ms_per_step": per_call,
+            "roofline": roofline, "stage_rooflines": stage_rooflines, "cpu_baseline": cpu, "flat_dsa": flat,
+            "stages_ms_per_step": per_call,
             "scorer_stall_fraction_of_cta_time": stalls,
             "candidate_pairs_per_step": cand_sum_all,
         }
