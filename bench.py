@@ -42,6 +42,8 @@ def parse_args():
     ap.add_argument("--cpu-rows", type=int, default=768, help="rows of the workload the CPU baseline is timed on")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--force-dist", action="store_true",
+                    help="initialise NCCL even with one rank (exercises the multi-GPU code path on a single GPU)")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp8"],
                     help="storage of q/k: bf16 (headline) or e4m3 with per-token key scales (query scales folded into the gates)")
     return ap.parse_args()
@@ -171,10 +173,12 @@ def run_b200(a, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
-    if world > 1:
+    if world > 1 or a.force_dist:
         import torch.distributed as dist_mod
         dist = dist_mod
-        dist.init_process_group("nccl", device_id=dev)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
 
     L = Q = a.seq_len
     H, d, B, m, k = 64, 128, a.block_size, a.block_budget, a.token_budget
@@ -212,7 +216,16 @@ def run_b200(a, rank, world, local_rank):
     out_idx = torch.empty((nq, k), device=dev, dtype=torch.int32)
     out_count = torch.empty((nq,), device=dev, dtype=torch.int32)
     out_cand = torch.empty((nq,), device=dev, dtype=torch.int32)
-    gathered = torch.empty((world * nq, k), device=dev, dtype=torch.int32) if dist else None
+    # multi-GPU: the rank's rows are selected in slices, and the all-gather of slice i (NCCL, its own stream) runs
+    # under the kernels of slice i+1 — at 8 GPUs the gather of the indices costs about half of the per-rank compute
+    # (SURVEY.md §8e), so it must not be serialised behind it
+    n_slices = 1 if not dist else (4 if nq > 8192 else 2)
+    step_rows = -(-nq // (n_slices * TILE_ROWS)) * TILE_ROWS
+    bounds = [min(i * step_rows, nq) for i in range(n_slices + 1)]
+    gathered = [torch.empty((world * (bounds[i + 1] - bounds[i]), k), device=dev, dtype=torch.int32)
+                for i in range(n_slices)] if dist else None
+    comm_stream = torch.cuda.Stream(device=dev) if dist else None
+    slice_done = [torch.cuda.Event() for _ in range(n_slices)] if dist else None
     torch.cuda.synchronize()
 
     cfg = capi.make_config(B, m, k, H, d, capi.DTYPE_FP8 if fp8 else capi.DTYPE_BF16)
@@ -223,11 +236,22 @@ def run_b200(a, rank, world, local_rank):
     stream = torch.cuda.ExternalStream(capi.lib().hisa_cuda_stream(ix._ctx), device=dev)
 
     def step_hisa():
-        ix.hisa_select_raw(q.data_ptr(), w.data_ptr(), pos.data_ptr(), nq, out_idx.data_ptr(), out_count.data_ptr(),
-                           None, None, out_cand.data_ptr())
-        if dist:
-            with torch.cuda.stream(stream):
-                dist.all_gather_into_tensor(gathered, out_idx)
+        if not dist:
+            ix.hisa_select_raw(q.data_ptr(), w.data_ptr(), pos.data_ptr(), nq, out_idx.data_ptr(), out_count.data_ptr(),
+                               None, None, out_cand.data_ptr())
+            return
+        for i in range(n_slices):
+            r0, r1 = bounds[i], bounds[i + 1]
+            if r1 <= r0:
+                continue
+            ix.hisa_select_raw(q[r0:r1].data_ptr(), w[r0:r1].data_ptr(), pos[r0:r1].data_ptr(), r1 - r0,
+                               out_idx[r0:r1].data_ptr(), out_count[r0:r1].data_ptr(), None, None,
+                               out_cand[r0:r1].data_ptr())
+            slice_done[i].record(stream)
+            with torch.cuda.stream(comm_stream):
+                comm_stream.wait_event(slice_done[i])
+                dist.all_gather_into_tensor(gathered[i], out_idx[r0:r1])
+        stream.wait_stream(comm_stream)  # the step ends when every rank holds every index row
 
     def step_flat():
         ix.dsa_select_raw(q.data_ptr(), w.data_ptr(), pos.data_ptr(), nq, out_idx.data_ptr(), out_count.data_ptr(), None)
@@ -283,7 +307,7 @@ def run_b200(a, rank, world, local_rank):
         cand_sum_all = cand_sum
     peaks = load_peaks()
     flops_s2 = 2.0 * d * H * cand_sum          # this rank, one launch
-    k_ms = stages["score_tokens_ms"] / max(stages["calls"], 1)
+    k_ms = stages["score_tokens_ms"] / a.steps   # per step (a step is several calls when the rows go in slices)
     achieved = flops_s2 / (k_ms * 1e-3) / 1e12 if k_ms > 0 else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic_score_tc_stage2_fp8.json" if a.dtype == "fp8" else "traffic_score_tc_stage2.json")
@@ -298,7 +322,7 @@ def run_b200(a, rank, world, local_rank):
                 "achieved": achieved, "peak": peaks["tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["tflops"], "traffic": traffic, "peak_source": peaks["source"],
                 "flops_per_launch": flops_s2, "kernel_ms": k_ms}
-    per_call = {kk: (vv / max(stages["calls"], 1) if kk.endswith("_ms") else vv) for kk, vv in stages.items()
+    per_call = {kk: (vv / a.steps if kk.endswith("_ms") else vv) for kk, vv in stages.items()
                 if kk != "stalls"}
     # ---- every stage against the roofline that bounds it (algorithmic work / CUDA-event time)
     pos64 = pos.to(torch.int64).clamp(max=L - 1)
