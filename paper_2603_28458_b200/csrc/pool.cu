@@ -137,12 +137,26 @@ pool_update_kernel(const __nv_bfloat16* __restrict__ key_op, uint32_t nseg_k, ui
   const bool fresh = (s_lo == blk_lo);
   double acc = fresh ? 0.0 : sums[b * kDim + c];
   const uint64_t row_elems = uint64_t(nseg_k) * kDim;
-  for (uint64_t s = s_lo; s < s_hi; ++s) {
-    const __nv_bfloat16* row = key_op + s * row_elems + c;
-    double v = 0.0;
-    for (uint32_t g = 0; g < nseg_k; ++g) v += double(__bfloat162float(row[g * kDim]));
-    if (pool_max) acc = (fresh && s == s_lo) ? v : (v > acc ? v : acc);
-    else acc += v;
+  // the adds stay in position order (bit-for-bit agreement with the incremental update and the CPU loop); the loads of
+  // eight rows are issued together so that one DRAM latency covers eight rows instead of one
+  constexpr int kAhead = 8;
+  for (uint64_t s0 = s_lo; s0 < s_hi; s0 += kAhead) {
+    double v[kAhead];
+#pragma unroll
+    for (int i = 0; i < kAhead; ++i) {
+      v[i] = 0.0;
+      if (s0 + i < s_hi) {
+        const __nv_bfloat16* row = key_op + (s0 + i) * row_elems + c;
+        for (uint32_t g = 0; g < nseg_k; ++g) v[i] += double(__bfloat162float(row[g * kDim]));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kAhead; ++i) {
+      if (s0 + i < s_hi) {
+        if (pool_max) acc = (fresh && s0 + i == s_lo) ? v[i] : (v[i] > acc ? v[i] : acc);
+        else acc += v[i];
+      }
+    }
   }
   sums[b * kDim + c] = acc;
   const uint32_t cnt = uint32_t(s_hi - blk_lo);
@@ -167,10 +181,19 @@ pool_update_fp8_kernel(const uint8_t* __restrict__ key8, const float* __restrict
   const uint64_t s_hi = (first + n) < blk_hi ? (first + n) : blk_hi;
   const bool fresh = (s_lo == blk_lo);
   double acc = fresh ? 0.0 : sums[b * kDim + c];
-  for (uint64_t s = s_lo; s < s_hi; ++s) {
-    const double v = double(e4m3_to_float(key8[s * kDim + c]) * key_scale[s]);
-    if (pool_max) acc = (fresh && s == s_lo) ? v : (v > acc ? v : acc);
-    else acc += v;
+  constexpr int kAhead = 8;  // loads of eight rows in flight, adds in position order (see pool_update_kernel)
+  for (uint64_t s0 = s_lo; s0 < s_hi; s0 += kAhead) {
+    double v[kAhead];
+#pragma unroll
+    for (int i = 0; i < kAhead; ++i)
+      v[i] = s0 + i < s_hi ? double(e4m3_to_float(key8[(s0 + i) * kDim + c]) * key_scale[s0 + i]) : 0.0;
+#pragma unroll
+    for (int i = 0; i < kAhead; ++i) {
+      if (s0 + i < s_hi) {
+        if (pool_max) acc = (fresh && s0 + i == s_lo) ? v[i] : (v[i] > acc ? v[i] : acc);
+        else acc += v[i];
+      }
+    }
   }
   sums[b * kDim + c] = acc;
   const uint32_t cnt = uint32_t(s_hi - blk_lo);
