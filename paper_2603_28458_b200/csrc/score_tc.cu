@@ -494,11 +494,6 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         reduce_frag(vx, gw[0], gw[1], a2, a3);
         tmem_ld_wait();
         if (act1) tmem_ld_16x128b_x8(t_lane + kHeads, vx);             // F(1, 0, 0)
-        if (a.debug_flags & 8u) {  // timing experiment only: hand the accumulator back half way (results are garbage)
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_addr(t_empty_addr);
-        }
         reduce_frag(vy, gw[2], gw[3], a2, a3);
         f.step1(a0, a1, a2, a3, b0);
         float* dst0 = a.out + uint64_t(qrows.x) * a.out_stride + qcols.x + row;
@@ -525,7 +520,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         // all dots of the group are in registers: hand the accumulator back to the MMA warp
         tc_fence_before();
         __syncwarp();
-        if (lane == 0 && !(a.debug_flags & 8u)) mbar_arrive_addr(t_empty_addr);
+        if (elect_one()) mbar_arrive_addr(t_empty_addr);
         if (act1) {
           reduce_frag(vy, gw[2], gw[3], a2, a3);
           f.step1(a0, a1, a2, a3, b0);
@@ -535,7 +530,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       } else {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_addr(t_empty_addr);
+        if (elect_one()) mbar_arrive_addr(t_empty_addr);
       }
     }
   }
