@@ -81,7 +81,7 @@ struct hisa_cuda_ctx {
 
   // host-buffer pipeline (select_impl): slices of pipe_rows rows are staged through double-buffered device
   // arrays so that the H2D copy of slice i+1 and the D2H copy of slice i-1 overlap the kernels of slice i
-  uint32_t pipe_rows = 2048;
+  uint32_t pipe_rows = 4096;
   bool pipe_ready = false;
   cudaStream_t in_stream = nullptr, out_stream = nullptr;
   cudaEvent_t ev_in_ready[2]{}, ev_in_free[2]{}, ev_out_ready[2]{}, ev_out_free[2]{};
@@ -925,7 +925,7 @@ int hisa_cuda_create(int device, const hisa_cuda_config* cfg, hisa_cuda_ctx** ou
   ctx->chunk_dense = std::max<uint32_t>(env_u32("HISA_CHUNK_DENSE", 256), 4);
   ctx->chunk_list = std::max<uint32_t>(env_u32("HISA_CHUNK_LIST", 512), 4);
   ctx->workspace_bytes = uint64_t(std::max<uint32_t>(env_u32("HISA_WORKSPACE_MB", 4096), 16)) << 20;
-  ctx->pipe_rows = env_u32("HISA_PIPE_ROWS", 2048);  // 0 disables the host-buffer pipeline
+  ctx->pipe_rows = env_u32("HISA_PIPE_ROWS", 4096);  // 0 disables the host-buffer pipeline
   *out = ctx;
   return HISA_OK;
 }
