@@ -14,6 +14,9 @@
  *   hisa_cuda_hisa_select        <- hisa::hisa_select       (hisa/hisa.hpp:35-45) incl. candidate_union (:30-33)
  *   hisa_cuda_dsa_select         <- hisa::dsa_select        (hisa/dsa.hpp:29-32)
  *   hisa_cuda_block_sparse_select<- hisa::block_sparse_select (hisa/block_sparse.hpp:12-19)
+ *   hisa_cuda_attn_set_latents   <- hisa::AttentionInputs   (hisa/attention.hpp:16-46), latent_states part
+ *   hisa_cuda_sparse_attend      <- hisa::sparse_attend     (hisa/attention.hpp:48-56), the step after the path
+ *   hisa_cuda_dense_attend       <- hisa::dense_attend      (hisa/attention.hpp:58-59)
  *   hisa_cuda_config             <- hisa::HisaConfig        (hisa/config.hpp:26-67), POD mirror
  *   status codes                 <- the exception leaves of hisa/errors.hpp:10-28
  *
@@ -184,6 +187,27 @@ int hisa_cuda_score_tokens(hisa_cuda_ctx* ctx, const void* queries, const float*
  * out_idx int32 [Q, k]. */
 int hisa_cuda_top_k(hisa_cuda_ctx* ctx, const float* scores, uint64_t score_stride, const uint32_t* n,
                     uint64_t num_rows, uint32_t k, int32_t* out_idx, uint32_t* out_count);
+
+/* ---- downstream consumer: attention over the selected tokens (hisa/attention.hpp:13-59, Eq.3) ----- */
+/* Stores latent_states [seq_len, d_model] (HISA_DTYPE_F32 or HISA_DTYPE_BF16; one latent per token acts as key and
+ * value). d_model <= 512. Independent of the indexer keys of the context. check_finite != 0 scans for NaN/Inf. */
+int hisa_cuda_attn_set_latents(hisa_cuda_ctx* ctx, const void* latent_states, uint64_t seq_len, uint32_t d_model,
+                               uint32_t dtype, int check_finite);
+/* u_t = sum_{s in T_t} softmax_s(scale * h_t . c_s) * c_s with the softmax normalised over T_t only.
+ * query_states [Q, d_model] of q_dtype (F32 or BF16), positions [Q] (each < seq_len),
+ * selected int32 [Q, sel_stride]: exactly the out_idx matrix of hisa_cuda_*_select (negative entries are padding),
+ * counts [Q] entries to read per row (NULL: all sel_stride entries, padding skipped),
+ * scale <= 0 selects 1/sqrt(d_model).  out float32 [Q, d_model]; weights float32 [Q, sel_stride] (optional,
+ * selection order, sum to 1, zero on padding).
+ * HISA_ERR_EMPTY_SELECTION if a row selects nothing, HISA_ERR_CAUSAL_VIOLATION if an index exceeds the row's position. */
+int hisa_cuda_sparse_attend(hisa_cuda_ctx* ctx, const void* query_states, uint32_t q_dtype, const uint32_t* positions,
+                            uint64_t num_queries, const int32_t* selected, uint64_t sel_stride, const uint32_t* counts,
+                            double scale, float* out, float* weights);
+/* Causal softmax attention over the whole prefix [0, t] of every row (the sparse = dense identity oracle). */
+int hisa_cuda_dense_attend(hisa_cuda_ctx* ctx, const void* query_states, uint32_t q_dtype, const uint32_t* positions,
+                           uint64_t num_queries, double scale, float* out);
+/* device time of the attention kernel of the last sparse/dense attend call (CUDA events on the context's stream) */
+int hisa_cuda_attn_last_ms(hisa_cuda_ctx* ctx, float* ms);
 
 /* ---- instrumentation --------------------------------------------------------------------------- */
 typedef struct hisa_cuda_stage_times {

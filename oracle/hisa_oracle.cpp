@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <numeric>
 
 namespace hisa_oracle {
@@ -468,6 +469,78 @@ OwnedInputs make_clustered_inputs(Rng& rng, uint32_t L, uint32_t Q, uint32_t H, 
         o.keys[size_t(p) * d + i] = float(double(o.keys[size_t(p) * d + i]) + span_boost * dir[i]);
   }
   return o;
+}
+
+// ---- downstream consumer: shared-KV softmax attention over a selection (attention.hpp:13-59) ----
+double AttnInputs::effective_scale() const {
+  return scale > 0.0 ? scale : 1.0 / std::sqrt(double(d_model));  // attention.hpp:20-21
+}
+
+void AttnInputs::validate() const {
+  if (d_model == 0) throw OracleError(Err::DimensionMismatch, "attention: d_model must be positive");
+  if (L == 0) throw OracleError(Err::EmptySequence, "attention: empty latent sequence");
+  for (size_t i = 0; i < size_t(Q) * d_model; ++i)
+    if (!std::isfinite(query_states[i])) throw OracleError(Err::NonFiniteValue, "attention: non-finite query state");
+  for (size_t i = 0; i < size_t(L) * d_model; ++i)
+    if (!std::isfinite(latent_states[i])) throw OracleError(Err::NonFiniteValue, "attention: non-finite latent state");
+  for (uint32_t r = 0; r < Q; ++r)
+    if (positions[r] >= L)  // attention.hpp:19-20: every position < L
+      throw OracleError(Err::ShapeMismatch, "attention: query position " + std::to_string(positions[r]) +
+                                                " is not below seq_len " + std::to_string(L));
+}
+
+namespace {
+// u = sum_i softmax_i(scale * h.c_{s_i}) * c_{s_i}, all arithmetic in double, max-subtracted
+std::vector<float> attend_over(const AttnInputs& a, uint32_t row, size_t n, const uint32_t* selected,
+                               std::vector<double>* weights_out) {
+  const uint32_t dm = a.d_model;
+  const float* h = a.query_states + size_t(row) * dm;
+  const double scale = a.effective_scale();
+  std::vector<double> logit(n);
+  double mx = -std::numeric_limits<double>::infinity();
+  for (size_t i = 0; i < n; ++i) {
+    const uint32_t s = selected ? selected[i] : uint32_t(i);
+    const float* c = a.latent_states + size_t(s) * dm;
+    double acc = 0.0;
+    for (uint32_t e = 0; e < dm; ++e) acc += double(h[e]) * double(c[e]);
+    logit[i] = scale * acc;
+    mx = std::max(mx, logit[i]);
+  }
+  double denom = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    logit[i] = std::exp(logit[i] - mx);
+    denom += logit[i];
+  }
+  std::vector<double> u(dm, 0.0);
+  for (size_t i = 0; i < n; ++i) {
+    const uint32_t s = selected ? selected[i] : uint32_t(i);
+    const float* c = a.latent_states + size_t(s) * dm;
+    const double w = logit[i] / denom;
+    logit[i] = w;
+    for (uint32_t e = 0; e < dm; ++e) u[e] += w * double(c[e]);
+  }
+  if (weights_out) *weights_out = std::move(logit);
+  std::vector<float> out(dm);
+  for (uint32_t e = 0; e < dm; ++e) out[e] = float(u[e]);
+  return out;
+}
+}  // namespace
+
+std::vector<float> sparse_attend(const AttnInputs& a, const uint32_t* selected, size_t n, uint32_t row,
+                                 std::vector<double>* weights_out) {
+  if (row >= a.Q) throw OracleError(Err::InvalidArgument, "sparse_attend: query_row out of range");
+  if (n == 0) throw OracleError(Err::EmptySelection, "sparse_attend: empty selection");  // attention.hpp:51
+  const uint32_t t = a.positions[row];
+  for (size_t i = 0; i < n; ++i)
+    if (selected[i] > t || selected[i] >= a.L)  // attention.hpp:52
+      throw OracleError(Err::CausalViolation, "sparse_attend: index " + std::to_string(selected[i]) +
+                                                  " exceeds query position " + std::to_string(t));
+  return attend_over(a, row, n, selected, weights_out);
+}
+
+std::vector<float> dense_attend(const AttnInputs& a, uint32_t row) {
+  if (row >= a.Q) throw OracleError(Err::InvalidArgument, "dense_attend: query_row out of range");
+  return attend_over(a, row, size_t(a.positions[row]) + 1, nullptr, nullptr);
 }
 
 }  // namespace hisa_oracle

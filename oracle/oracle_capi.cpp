@@ -314,4 +314,33 @@ int horacle_trace_row(int strategy, const Problem* p, uint32_t row, double* J, u
   });
 }
 
+// ---- downstream consumer (attention.hpp:48-59). selected == NULL: dense_attend over [0, t] of every row.
+// selected int32 [nrows, sel_stride] (-1 padded), counts [nrows]; out float [nrows, d_model];
+// weights (optional) double [nrows, sel_stride], selection order. Row r of the batch is query row rows[r] (or r).
+int horacle_attend_batch(const float* query_states, const float* latent_states, const uint32_t* positions, uint32_t Q,
+                         uint32_t L, uint32_t d_model, double scale, const uint32_t* rows, uint32_t nrows,
+                         const int32_t* selected, uint32_t sel_stride, const uint32_t* counts, uint32_t threads,
+                         float* out, double* weights) {
+  return guarded([&] {
+    AttnInputs a;
+    a.query_states = query_states; a.latent_states = latent_states; a.positions = positions;
+    a.Q = Q; a.L = L; a.d_model = d_model; a.scale = scale;
+    a.validate();
+    parallel_rows(nrows, threads ? threads : horacle_hardware_threads(), [&](size_t i) {
+      const uint32_t row = rows ? rows[i] : uint32_t(i);
+      std::vector<float> u;
+      if (selected) {
+        std::vector<uint32_t> sel(counts[i]);
+        for (uint32_t j = 0; j < counts[i]; ++j) sel[j] = uint32_t(selected[size_t(i) * sel_stride + j]);
+        std::vector<double> w;
+        u = sparse_attend(a, sel.data(), sel.size(), row, weights ? &w : nullptr);
+        if (weights) std::memcpy(weights + size_t(i) * sel_stride, w.data(), w.size() * sizeof(double));
+      } else {
+        u = dense_attend(a, row);
+      }
+      std::memcpy(out + size_t(i) * d_model, u.data(), d_model * sizeof(float));
+    });
+  });
+}
+
 }  // extern "C"

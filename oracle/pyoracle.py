@@ -301,3 +301,32 @@ def trace_row(strategy: str, p: Problem, row: int):
     _check(lib().horacle_trace_row(C.c_int(STRATEGY[strategy]), C.byref(s), C.c_uint32(row), _p(J), C.byref(nJ), _p(blocks),
                                    C.byref(nb), _p(omega), _p(scores), C.byref(no)))
     return {"J": J[:nJ.value], "blocks": blocks[:nb.value], "omega": omega[:no.value], "omega_scores": scores[:no.value]}
+
+
+def attend_batch(query_states, latent_states, positions, selected=None, counts=None, rows=None, scale: float = 0.0,
+                 threads: int = 0, want_weights: bool = False):
+    """sparse_attend (selected int32 [n, stride] -1 padded + counts [n]) or dense_attend (selected=None) for the
+    query rows `rows` (default all). attention.hpp:48-59. -> out f32 [n, d_model] (, weights f64 [n, stride])."""
+    qs = np.ascontiguousarray(query_states, dtype=np.float32)
+    ls = np.ascontiguousarray(latent_states, dtype=np.float32)
+    pos = np.ascontiguousarray(positions, dtype=np.uint32)
+    Q, dm = qs.shape
+    L = ls.shape[0]
+    if rows is None:
+        rows = np.arange(Q, dtype=np.uint32)
+    rows = np.ascontiguousarray(rows, dtype=np.uint32)
+    n = rows.shape[0]
+    out = np.zeros((n, dm), np.float32)
+    weights = None
+    stride = 0
+    if selected is not None:
+        selected = np.ascontiguousarray(selected, dtype=np.int32)
+        counts = np.ascontiguousarray(counts, dtype=np.uint32)
+        assert selected.shape[0] == n and counts.shape[0] == n
+        stride = selected.shape[1]
+        if want_weights:
+            weights = np.zeros((n, stride), np.float64)
+    _check(lib().horacle_attend_batch(_p(qs), _p(ls), _p(pos), C.c_uint32(Q), C.c_uint32(L), C.c_uint32(dm),
+                                      C.c_double(scale), _p(rows), C.c_uint32(n), _p(selected), C.c_uint32(stride),
+                                      _p(counts), C.c_uint32(threads), _p(out), _p(weights)))
+    return (out, weights) if want_weights else out

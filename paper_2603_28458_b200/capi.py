@@ -29,6 +29,7 @@ EXPORTED_SYMBOLS = [
     "hisa_cuda_hisa_select", "hisa_cuda_dsa_select", "hisa_cuda_block_sparse_select", "hisa_cuda_score_blocks",
     "hisa_cuda_select_blocks", "hisa_cuda_score_tokens", "hisa_cuda_top_k", "hisa_cuda_set_profiling",
     "hisa_cuda_last_stage_times", "hisa_cuda_launch_count", "hisa_cuda_scorer_stall_cycles",
+    "hisa_cuda_attn_set_latents", "hisa_cuda_sparse_attend", "hisa_cuda_dense_attend", "hisa_cuda_attn_last_ms",
 ]
 
 
@@ -382,6 +383,54 @@ class Indexer:
         _check(lib().hisa_cuda_top_k(self._ctx, _ptr(scores), C.c_uint64(scores.shape[1]), _ptr(n), C.c_uint64(rows), C.c_uint32(k),
                                      _ptr(idx), _ptr(cnt)), self._ctx)
         return idx, cnt
+
+    # -- downstream consumer (attention.hpp:13-59)
+    @staticmethod
+    def _attn_elems(a):
+        """numpy -> (array, dtype code): uint16 arrays are bf16 bit patterns, everything else becomes float32."""
+        if isinstance(a, np.ndarray) and a.dtype == np.uint16:
+            return np.ascontiguousarray(a), DTYPE_BF16
+        return np.ascontiguousarray(a, dtype=np.float32), DTYPE_F32
+
+    def attn_set_latents(self, latent_states, check_finite=False):
+        lat, dt = self._attn_elems(latent_states)
+        L, dm = lat.shape
+        _check(lib().hisa_cuda_attn_set_latents(self._ctx, _ptr(lat), C.c_uint64(L), C.c_uint32(dm), C.c_uint32(dt),
+                                                C.c_int(int(check_finite))), self._ctx)
+        self._attn_dm = dm
+
+    def sparse_attend(self, query_states, positions, selected, counts=None, scale=0.0, want_weights=False):
+        qs, dt = self._attn_elems(query_states)
+        pos = np.ascontiguousarray(positions, dtype=np.uint32)
+        sel = np.ascontiguousarray(selected, dtype=np.int32).reshape(pos.shape[0], -1)
+        cnt = None if counts is None else np.ascontiguousarray(counts, dtype=np.uint32)
+        Q = pos.shape[0]
+        out = np.zeros((Q, self._attn_dm), np.float32)
+        weights = np.zeros(sel.shape, np.float32) if want_weights else None
+        _check(lib().hisa_cuda_sparse_attend(self._ctx, _ptr(qs), C.c_uint32(dt), _ptr(pos), C.c_uint64(Q), _ptr(sel),
+                                             C.c_uint64(sel.shape[1]), _ptr(cnt), C.c_double(scale), _ptr(out),
+                                             _ptr(weights)), self._ctx)
+        return (out, weights) if want_weights else out
+
+    def dense_attend(self, query_states, positions, scale=0.0):
+        qs, dt = self._attn_elems(query_states)
+        pos = np.ascontiguousarray(positions, dtype=np.uint32)
+        Q = pos.shape[0]
+        out = np.zeros((Q, self._attn_dm), np.float32)
+        _check(lib().hisa_cuda_dense_attend(self._ctx, _ptr(qs), C.c_uint32(dt), _ptr(pos), C.c_uint64(Q), C.c_double(scale),
+                                            _ptr(out)), self._ctx)
+        return out
+
+    def sparse_attend_raw(self, q, q_dtype, pos, Q, selected, sel_stride, counts, out, scale=0.0, weights=None):
+        """device / pinned-host addresses only; nothing is allocated or copied here"""
+        _check(lib().hisa_cuda_sparse_attend(self._ctx, _ptr(q), C.c_uint32(q_dtype), _ptr(pos), C.c_uint64(Q), _ptr(selected),
+                                             C.c_uint64(sel_stride), _ptr(counts), C.c_double(scale), _ptr(out),
+                                             _ptr(weights)), self._ctx)
+
+    def attn_last_ms(self) -> float:
+        ms = C.c_float(0.0)
+        _check(lib().hisa_cuda_attn_last_ms(self._ctx, C.byref(ms)), self._ctx)
+        return ms.value
 
 
 def host_alloc(nbytes: int) -> int:

@@ -7,6 +7,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -60,6 +61,14 @@ struct hisa_cuda_ctx {
   // per-call workspace
   DevBuf q_raw, q_op, gates_raw, gates_pad, pos, J, sel, nsel, work, pairs, scalars, cand, flat, out_idx, out_count,
       out_cand, generic_scores, generic_n, export_a, export_b, flag, stats;
+
+  // downstream consumer (attention.hpp): latent table + per-call staging
+  DevBuf attn_lat, attn_q, attn_qraw, attn_pos, attn_idx, attn_cnt, attn_out, attn_w;
+  uint64_t attn_len = 0;
+  uint32_t attn_dm = 0, attn_dm_pad = 0;
+  bool attn_bf16 = false;
+  cudaEvent_t attn_beg = nullptr, attn_end = nullptr;
+  bool attn_timed = false;
 
   // tuning
   uint32_t chunk_dense = 256, chunk_list = 512;
@@ -937,8 +946,12 @@ int hisa_cuda_destroy(hisa_cuda_ctx* ctx) {
   for (DevBuf* b : {&ctx->key_op, &ctx->key_raw, &ctx->key_scale, &ctx->sums, &ctx->counts, &ctx->pooled_op, &ctx->q_raw, &ctx->q_op,
                     &ctx->gates_raw, &ctx->gates_pad, &ctx->pos, &ctx->J, &ctx->sel, &ctx->nsel, &ctx->work, &ctx->pairs,
                     &ctx->scalars, &ctx->cand, &ctx->flat, &ctx->out_idx, &ctx->out_count, &ctx->out_cand,
-                    &ctx->generic_scores, &ctx->generic_n, &ctx->export_a, &ctx->export_b, &ctx->flag, &ctx->stats})
+                    &ctx->generic_scores, &ctx->generic_n, &ctx->export_a, &ctx->export_b, &ctx->flag, &ctx->stats,
+                    &ctx->attn_lat, &ctx->attn_q, &ctx->attn_qraw, &ctx->attn_pos, &ctx->attn_idx, &ctx->attn_cnt,
+                    &ctx->attn_out, &ctx->attn_w})
     release(*b);
+  if (ctx->attn_beg) cudaEventDestroy(ctx->attn_beg);
+  if (ctx->attn_end) cudaEventDestroy(ctx->attn_end);
   for (int i = 0; i < 2; ++i)
     for (DevBuf* b : {&ctx->st_q[i], &ctx->st_g[i], &ctx->st_pos[i], &ctx->st_idx[i], &ctx->st_cnt[i], &ctx->st_cand[i],
                       &ctx->st_blk[i], &ctx->st_nblk[i]})
@@ -1328,6 +1341,168 @@ int hisa_cuda_score_tokens(hisa_cuda_ctx* ctx, const void* queries, const float*
                                   cudaMemcpyDefault, ctx->stream));
   end_call(ctx);
   CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return HISA_OK;
+}
+
+// ---- downstream consumer: attention over the selection (attention.hpp:13-59) -------------------------------
+
+int hisa_cuda_attn_set_latents(hisa_cuda_ctx* ctx, const void* latents, uint64_t seq_len, uint32_t d_model, uint32_t dtype,
+                               int check_finite) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  if (dtype != HISA_DTYPE_F32 && dtype != HISA_DTYPE_BF16)
+    return fail(ctx, HISA_ERR_UNSUPPORTED, "attention: latent_states must be float32 or bfloat16");
+  if (d_model == 0) return fail(ctx, HISA_ERR_DIMENSION_MISMATCH, "attention: d_model must be positive");
+  if (seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "attention: empty latent sequence");
+  if (seq_len > 0x7FFFFFFFull) return fail(ctx, HISA_ERR_UNSUPPORTED, "attention: seq_len beyond int32 indices");
+  if (!latents) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "attention: null latent_states");
+  const bool bf16 = dtype == HISA_DTYPE_BF16;
+  const uint32_t dm_pad = attend_padded_dim(d_model, bf16);
+  if (!dm_pad) return fail(ctx, HISA_ERR_UNSUPPORTED, "attention: d_model %u > 512", d_model);
+  const size_t eb = bf16 ? 2 : 4;
+  ctx->attn_len = 0;
+  HISA_TRY(ensure(ctx, ctx->attn_lat, size_t(seq_len) * dm_pad * eb));
+  const void* src = latents;
+  const bool direct = dm_pad == d_model;  // already in the kernel's layout: one copy, no padding pass
+  if (!is_device_ptr(latents)) {
+    void* stage = ctx->attn_lat.p;
+    if (!direct) {
+      HISA_TRY(ensure(ctx, ctx->attn_qraw, size_t(seq_len) * d_model * eb));
+      stage = ctx->attn_qraw.p;
+    }
+    HISA_TRY(copy_in(ctx, stage, latents, size_t(seq_len) * d_model * eb));
+    src = stage;
+  } else if (direct) {
+    HISA_TRY(copy_in(ctx, ctx->attn_lat.p, latents, size_t(seq_len) * d_model * eb));
+    src = ctx->attn_lat.p;
+  }
+  if (check_finite) {
+    HISA_TRY(ensure(ctx, ctx->flag, 64));
+    CU_TRY(ctx, cudaMemsetAsync(ctx->flag.p, 0, 64, ctx->stream));
+    count_launches(ctx, launch_check_finite(src, bf16 ? 1u : 0u, seq_len * d_model, ctx->flag.as<uint32_t>(), ctx->stream));
+    uint32_t bad = 0;
+    HISA_TRY(read_flag(ctx, &bad));
+    if (bad) return fail(ctx, HISA_ERR_NON_FINITE, "attention: non-finite value in latent_states");
+  }
+  if (!direct)
+    count_launches(ctx, launch_pad_rows(src, bf16, seq_len, d_model, dm_pad, ctx->attn_lat.p, bf16, ctx->stream));
+  HISA_TRY(check_launch(ctx, "latent ingestion"));
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->attn_len = seq_len;
+  ctx->attn_dm = d_model;
+  ctx->attn_dm_pad = dm_pad;
+  ctx->attn_bf16 = bf16;
+  return HISA_OK;
+}
+
+static int attend_impl(hisa_cuda_ctx* ctx, const void* query_states, uint32_t q_dtype, const uint32_t* positions, uint64_t Q,
+                       const int32_t* selected, uint64_t sel_stride, const uint32_t* counts, bool dense, double scale,
+                       float* out, float* weights) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  if (ctx->attn_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "attention: no latent_states (hisa_cuda_attn_set_latents)");
+  if (q_dtype != HISA_DTYPE_F32 && q_dtype != HISA_DTYPE_BF16)
+    return fail(ctx, HISA_ERR_UNSUPPORTED, "attention: query_states must be float32 or bfloat16");
+  ctx->attn_timed = false;
+  if (Q == 0) return HISA_OK;
+  if (Q > 0xFFFFFFFFull) return fail(ctx, HISA_ERR_UNSUPPORTED, "attention: too many rows in one call");
+  if (!query_states || !positions || !out) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "attention: null argument");
+  if (!dense && !selected) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "sparse_attend: null selection");
+  if (!dense && sel_stride == 0) return fail(ctx, HISA_ERR_EMPTY_SELECTION, "sparse_attend: empty selection");
+  const uint32_t dm = ctx->attn_dm, dmp = ctx->attn_dm_pad;
+  const bool qbf = q_dtype == HISA_DTYPE_BF16;
+  const size_t qeb = qbf ? 2 : 4;
+  // query states -> f32 [Q, dm_pad]
+  const void* q_dev = query_states;
+  if (!is_device_ptr(query_states)) {
+    HISA_TRY(ensure(ctx, ctx->attn_qraw, size_t(Q) * dm * qeb));
+    HISA_TRY(copy_in(ctx, ctx->attn_qraw.p, query_states, size_t(Q) * dm * qeb));
+    q_dev = ctx->attn_qraw.p;
+  }
+  if (qbf || dm != dmp) {
+    HISA_TRY(ensure(ctx, ctx->attn_q, size_t(Q) * dmp * 4));
+    count_launches(ctx, launch_pad_rows(q_dev, qbf, Q, dm, dmp, ctx->attn_q.p, false, ctx->stream));
+    q_dev = ctx->attn_q.p;
+  }
+  auto stage_in = [&](DevBuf& buf, const void* p, size_t bytes, const void** dev) -> int {
+    *dev = p;
+    if (p && !is_device_ptr(p)) {
+      HISA_TRY(ensure(ctx, buf, bytes));
+      HISA_TRY(copy_in(ctx, buf.p, p, bytes));
+      *dev = buf.p;
+    }
+    return HISA_OK;
+  };
+  const void *pos_dev = nullptr, *idx_dev = nullptr, *cnt_dev = nullptr;
+  HISA_TRY(stage_in(ctx->attn_pos, positions, Q * 4, &pos_dev));
+  if (!dense) {
+    HISA_TRY(stage_in(ctx->attn_idx, selected, Q * sel_stride * 4, &idx_dev));
+    HISA_TRY(stage_in(ctx->attn_cnt, counts, Q * 4, &cnt_dev));
+  }
+  const bool out_dev = is_device_ptr(out), w_dev = weights && is_device_ptr(weights);
+  if (!out_dev) HISA_TRY(ensure(ctx, ctx->attn_out, Q * dm * 4));
+  if (weights && !w_dev) HISA_TRY(ensure(ctx, ctx->attn_w, Q * sel_stride * 4));
+  HISA_TRY(ensure(ctx, ctx->flag, 64));
+  CU_TRY(ctx, cudaMemsetAsync(ctx->flag.p, 0, 64, ctx->stream));
+  AttendArgs a{};
+  a.latents = ctx->attn_lat.p;
+  a.queries = static_cast<const float*>(q_dev);
+  a.pos = static_cast<const uint32_t*>(pos_dev);
+  a.idx = static_cast<const int32_t*>(idx_dev);
+  a.count = static_cast<const uint32_t*>(cnt_dev);
+  a.idx_stride = dense ? 0 : sel_stride;
+  a.num_rows = uint32_t(Q);
+  a.seq_len = uint32_t(ctx->attn_len);
+  a.d_model = dm;
+  a.dm_pad = dmp;
+  a.latents_bf16 = ctx->attn_bf16 ? 1u : 0u;
+  a.scale = float(scale > 0.0 ? scale : 1.0 / std::sqrt(double(dm)));  // attention.hpp:20-21
+  a.out = out_dev ? out : ctx->attn_out.as<float>();
+  a.weights = !weights || dense ? nullptr : (w_dev ? weights : ctx->attn_w.as<float>());
+  a.weights_stride = sel_stride;
+  a.flag = ctx->flag.as<uint32_t>();
+  if (!ctx->attn_beg) {
+    CU_TRY(ctx, cudaEventCreate(&ctx->attn_beg));
+    CU_TRY(ctx, cudaEventCreate(&ctx->attn_end));
+  }
+  CU_TRY(ctx, cudaEventRecord(ctx->attn_beg, ctx->stream));
+  const int launched = launch_sparse_attend(a, ctx->stream);
+  CU_TRY(ctx, cudaEventRecord(ctx->attn_end, ctx->stream));
+  if (!launched) return fail(ctx, HISA_ERR_UNSUPPORTED, "attention: no kernel for d_model %u", dm);
+  count_launches(ctx, launched);
+  HISA_TRY(check_launch(ctx, "sparse_attend"));
+  ctx->attn_timed = true;
+  uint32_t flags = 0;
+  HISA_TRY(read_flag(ctx, &flags));
+  if (flags & 4u) return fail(ctx, HISA_ERR_SHAPE_MISMATCH, "attention: a query position is not below seq_len %llu",
+                              (unsigned long long)ctx->attn_len);
+  if (flags & 2u) return fail(ctx, HISA_ERR_CAUSAL_VIOLATION, "sparse_attend: a selected index exceeds its query position");
+  if (flags & 1u) return fail(ctx, HISA_ERR_EMPTY_SELECTION, "sparse_attend: empty selection");
+  bool need_sync = false;
+  if (!out_dev) HISA_TRY(copy_out(ctx, out, a.out, Q * dm * 4, &need_sync));
+  if (a.weights && !w_dev) HISA_TRY(copy_out(ctx, weights, a.weights, Q * sel_stride * 4, &need_sync));
+  if (need_sync) CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return HISA_OK;
+}
+
+int hisa_cuda_sparse_attend(hisa_cuda_ctx* ctx, const void* query_states, uint32_t q_dtype, const uint32_t* positions,
+                            uint64_t num_queries, const int32_t* selected, uint64_t sel_stride, const uint32_t* counts,
+                            double scale, float* out, float* weights) {
+  return attend_impl(ctx, query_states, q_dtype, positions, num_queries, selected, sel_stride, counts, false, scale, out,
+                     weights);
+}
+
+int hisa_cuda_dense_attend(hisa_cuda_ctx* ctx, const void* query_states, uint32_t q_dtype, const uint32_t* positions,
+                           uint64_t num_queries, double scale, float* out) {
+  return attend_impl(ctx, query_states, q_dtype, positions, num_queries, nullptr, 0, nullptr, true, scale, out, nullptr);
+}
+
+int hisa_cuda_attn_last_ms(hisa_cuda_ctx* ctx, float* ms) {
+  if (!ctx || !ms) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "null argument");
+  *ms = 0.f;
+  if (!ctx->attn_timed) return HISA_OK;
+  CU_TRY(ctx, cudaEventSynchronize(ctx->attn_end));
+  CU_TRY(ctx, cudaEventElapsedTime(ms, ctx->attn_beg, ctx->attn_end));
   return HISA_OK;
 }
 

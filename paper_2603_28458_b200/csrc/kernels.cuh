@@ -115,7 +115,30 @@ struct SelectArgs {
   uint32_t* out_cand;
 };
 
+// sparse_attend / dense_attend (attention.hpp:48-59): one warp per query row
+struct AttendArgs {
+  const void* latents;    // [seq_len, dm_pad] f32 or bf16 (zero padded beyond d_model)
+  const float* queries;   // [num_rows, dm_pad] f32 query states (zero padded)
+  const uint32_t* pos;    // [num_rows] query positions, each < seq_len
+  const int32_t* idx;     // [num_rows, idx_stride] selected tokens (negative = padding); null = whole prefix [0, t]
+  const uint32_t* count;  // [num_rows] entries of idx to read per row; null = idx_stride
+  uint64_t idx_stride;
+  uint32_t num_rows, seq_len, d_model, dm_pad;
+  uint32_t latents_bf16;
+  float scale;
+  float* out;             // [num_rows, d_model]
+  float* weights;         // optional [num_rows, weights_stride], selection order, zero beyond the row's count
+  uint64_t weights_stride;
+  uint32_t* flag;         // device word, OR of: 1 empty selection, 2 causal violation, 4 position >= seq_len
+};
+
 // ---- launchers (each returns the number of kernels it launched) ---------------------------------
+// padded model dimension the attention kernel works on (32 * 2^i, at most 512); 0 = unsupported
+uint32_t attend_padded_dim(uint32_t d_model, bool bf16);
+int launch_sparse_attend(const AttendArgs& args, cudaStream_t stream);
+int launch_pad_rows(const void* src, bool src_bf16, uint64_t rows, uint32_t dim, uint32_t dim_pad, void* dst,
+                    bool dst_bf16, cudaStream_t stream);
+
 int launch_score_tc(const ScoreArgs& args, const CUtensorMap& map_a, const CUtensorMap& map_b, int num_sms,
                     cudaStream_t stream);
 int launch_score_simt(const ScoreArgs& args, const __nv_bfloat16* a_op, const __nv_bfloat16* q_op,
