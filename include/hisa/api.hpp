@@ -277,6 +277,88 @@ BenchRecord run_bench(const HisaConfig& cfg, uint32_t seq_len, uint32_t num_quer
 void write_bench_csv(std::ostream& os, const std::vector<BenchRecord>& records);
 
 // ---------------------------------------------------------------------------------------------------
+// downstream consumer — reference: hisa/attention.hpp:13-59 (softmax attention over the selected tokens; one latent
+// per token acts as key and value). sparse_attend / dense_attend run on the device (hisa_cuda_sparse_attend).
+// ---------------------------------------------------------------------------------------------------
+class AttentionInputs {
+ public:
+  // query_states [Q, d_model], latent_states [L, d_model], query_positions [Q] with every position < L;
+  // scale <= 0 selects 1/sqrt(d_model). Rejects NaN/Inf (NonFiniteValue) and inconsistent shapes (ShapeMismatch).
+  AttentionInputs(std::vector<float> query_states, std::vector<float> latent_states,
+                  std::vector<uint32_t> query_positions, uint32_t d_model, double scale = 0.0);
+
+  uint32_t num_queries() const { return static_cast<uint32_t>(query_positions_.size()); }
+  uint32_t seq_len() const { return seq_len_; }
+  uint32_t d_model() const { return d_model_; }
+  double scale() const { return scale_; }
+  std::span<const float> query_state(uint32_t row) const { return {&query_states_[std::size_t(row) * d_model_], d_model_}; }
+  std::span<const float> latent(uint32_t pos) const { return {&latent_states_[std::size_t(pos) * d_model_], d_model_}; }
+  uint32_t position(uint32_t row) const { return query_positions_[row]; }
+  const std::vector<float>& query_states_raw() const { return query_states_; }
+  const std::vector<float>& latent_states_raw() const { return latent_states_; }
+  const std::vector<uint32_t>& positions_raw() const { return query_positions_; }
+
+ private:
+  std::vector<float> query_states_, latent_states_;
+  std::vector<uint32_t> query_positions_;
+  uint32_t d_model_ = 0, seq_len_ = 0;
+  double scale_ = 0.0;
+};
+
+std::vector<float> sparse_attend(const AttentionInputs& attn, std::span<const uint32_t> selected, uint32_t query_row,
+                                 std::vector<double>* weights_out = nullptr);
+std::vector<float> sparse_attend(const AttentionInputs& attn, const SelectionResult& selection, uint32_t query_row,
+                                 std::vector<double>* weights_out = nullptr);
+std::vector<float> dense_attend(const AttentionInputs& attn, uint32_t query_row);
+
+// ---------------------------------------------------------------------------------------------------
+// self-checking audits — reference: hisa/audit.hpp:14-80. Every strategy call inside is a batched device call.
+// ---------------------------------------------------------------------------------------------------
+struct AuditFailure {
+  uint64_t instance_seed = 0;
+  uint32_t query_row = 0;
+  std::string detail;
+};
+struct AuditReport {
+  uint32_t instances_run = 0;
+  uint32_t queries_checked = 0;
+  bool failed = false;
+  AuditFailure failure;  // meaningful when failed
+  bool passed() const { return !failed; }
+};
+struct AuditOptions {
+  uint64_t base_seed = 1;
+  uint32_t min_queries = 1000;  // instances are generated until this many query checks ran
+  uint32_t threads = 0;         // unused on the device path (kept for source compatibility)
+  bool inject_tie_mismatch = false;  // fault injection: opposite tie-break on a tie-saturated instance
+};
+AuditReport run_regime_equivalence_audit(const AuditOptions& options);
+AuditReport run_dense_regime_audit(const AuditOptions& options);
+AuditReport run_subset_chain_audit(const AuditOptions& options);
+
+struct AblationConfig {
+  uint32_t block_size = 0;
+  uint32_t block_budget = 0;
+  bool token_refinement = true;  // false: block-sparse baseline
+};
+struct AblationRow {
+  AblationConfig config;
+  double mean_overlap = 0.0;
+  double min_overlap = 0.0;
+};
+struct AblationOptions {
+  std::vector<AblationConfig> configs = {{64, 128, true}, {128, 64, true}, {256, 32, true}, {128, 16, false}};
+  uint32_t seq_len = 16384;
+  uint32_t token_budget = 2048;
+  uint32_t num_heads = 4;
+  uint32_t dim = 64;
+  uint32_t seeds = 20;
+  uint64_t base_seed = 7;
+  uint32_t threads = 0;
+};
+std::vector<AblationRow> run_overlap_ablation(const AblationOptions& options);
+
+// ---------------------------------------------------------------------------------------------------
 // batched device entry points (new; a per-row device call is meaningless at scale)
 // ---------------------------------------------------------------------------------------------------
 namespace gpu {
@@ -316,6 +398,28 @@ class Indexer {
  private:
   void* ctx_ = nullptr;
   HisaConfig cfg_;
+  Storage storage_;
+};
+
+// Batched consumer: latents live on the device; one call attends all rows of `attn` over their selections.
+class Attention {
+ public:
+  explicit Attention(const AttentionInputs& attn, Storage storage = Storage::F32, int device = 0);
+  ~Attention();
+  Attention(const Attention&) = delete;
+  Attention& operator=(const Attention&) = delete;
+  // out [Q, d_model] row-major; selections[r] belongs to query row r. weights (optional): per row, selection order.
+  std::vector<float> sparse_attend_batch(const std::vector<SelectionResult>& selections,
+                                         std::vector<std::vector<double>>* weights_out = nullptr);
+  std::vector<float> sparse_attend_rows(std::span<const uint32_t> rows, const std::vector<std::span<const uint32_t>>& selected,
+                                        std::vector<std::vector<double>>* weights_out = nullptr);
+  std::vector<float> dense_attend_batch();
+  std::vector<float> dense_attend_rows(std::span<const uint32_t> rows);
+  float last_kernel_ms();
+
+ private:
+  void* ctx_ = nullptr;
+  const AttentionInputs* attn_;
   Storage storage_;
 };
 

@@ -8,6 +8,8 @@
 #include <numeric>
 #include <sstream>
 
+#include "hisa/attention.hpp"
+#include "hisa/audit.hpp"
 #include "hisa/block_sparse.hpp"
 #include "hisa/bench.hpp"
 #include "hisa/hisa.hpp"
@@ -213,6 +215,101 @@ int main() {
     EXPECT(throws<BadMagic>([&] { load_tensor_file(path); }));
     std::filesystem::remove(path);
     EXPECT(throws<IoError>([&] { load_tensor_file(path); }));
+  }
+  // ---- downstream consumer (attention.hpp:48-59) ----
+  {
+    Rng rng(21);
+    const uint32_t L = 512, Q = 6, dm = 24;
+    std::vector<float> lat(L * dm), hs(Q * dm);
+    for (auto& v : lat) v = float(rng.normal());
+    for (auto& v : hs) v = float(rng.normal());
+    const AttentionInputs attn(hs, lat, {0, 100, 200, 300, 400, 511}, dm);
+    EXPECT(std::abs(attn.scale() - 1.0 / std::sqrt(24.0)) < 1e-15);
+    // single token -> that latent exactly; L = 1 prefix -> c_0
+    const uint32_t one[] = {77};
+    auto u = sparse_attend(attn, one, 2);
+    EXPECT(std::equal(u.begin(), u.end(), attn.latent(77).begin()));
+    auto d0 = dense_attend(attn, 0);
+    EXPECT(std::equal(d0.begin(), d0.end(), attn.latent(0).begin()));
+    // full prefix == dense within 1e-5; weights sum to 1 within 1e-6 (fp32 device arithmetic: 1e-5)
+    std::vector<uint32_t> prefix(301);
+    std::iota(prefix.begin(), prefix.end(), 0u);
+    std::vector<double> w;
+    auto sp = sparse_attend(attn, prefix, 3, &w);
+    auto de = dense_attend(attn, 3);
+    double worst = 0, wsum = 0;
+    for (uint32_t i = 0; i < dm; ++i) worst = std::max(worst, double(std::abs(sp[i] - de[i])));
+    for (double x : w) wsum += x;
+    EXPECT(worst <= 1e-5 && w.size() == 301 && std::abs(wsum - 1.0) <= 1e-5);
+    // naive double-precision check of one row
+    {
+      std::vector<double> logit(301), ref(dm, 0.0);
+      double mx = -1e300, den = 0;
+      for (uint32_t s = 0; s <= 300; ++s) {
+        double acc = 0;
+        for (uint32_t i = 0; i < dm; ++i) acc += double(attn.query_state(3)[i]) * double(attn.latent(s)[i]);
+        logit[s] = acc * attn.scale();
+        mx = std::max(mx, logit[s]);
+      }
+      for (auto& x : logit) { x = std::exp(x - mx); den += x; }
+      for (uint32_t s = 0; s <= 300; ++s)
+        for (uint32_t i = 0; i < dm; ++i) ref[i] += logit[s] / den * double(attn.latent(s)[i]);
+      double err = 0;
+      for (uint32_t i = 0; i < dm; ++i) err = std::max(err, std::abs(ref[i] - double(de[i])));
+      EXPECT(err <= 1e-5);
+    }
+    EXPECT(throws<EmptySelection>([&] { sparse_attend(attn, std::span<const uint32_t>{}, 1); }));
+    const uint32_t future[] = {5, 101};
+    EXPECT(throws<CausalViolation>([&] { sparse_attend(attn, future, 1); }));
+    EXPECT(throws<ShapeMismatch>([&] { AttentionInputs bad(hs, lat, {0, 1, 2, 3, 4, 512}, dm); (void)bad; }));
+    // plug-and-play: the SelectionResult of every strategy feeds the consumer unchanged
+    Rng r2(22);
+    const HisaConfig cfg(32, 4, 64, 4, 16);
+    auto in = make_random_inputs(r2, L, std::vector<uint32_t>{0, 100, 200, 300, 400, 511}, 4, 16);
+    auto cache = build_block_summaries(in.keys_raw(), 16, 32);
+    for (uint32_t row = 0; row < Q; ++row) {
+      for (const SelectionResult& sel : {dsa_select(in, cfg, row), hisa_select(in, cache, cfg, row), block_sparse_select(in, cache, cfg, row)}) {
+        std::vector<double> ww;
+        auto out = sparse_attend(attn, sel, row, &ww);
+        double s1 = 0;
+        for (double x : ww) s1 += x;
+        EXPECT(out.size() == dm && ww.size() == sel.token_indices.size() && std::abs(s1 - 1.0) <= 1e-5);
+      }
+    }
+    gpu::Attention batched(attn, gpu::Storage::F32);
+    std::vector<SelectionResult> sels;
+    for (uint32_t row = 0; row < Q; ++row) sels.push_back(hisa_select(in, cache, cfg, row));
+    auto all = batched.sparse_attend_batch(sels);
+    auto row4 = sparse_attend(attn, sels[4], 4);
+    EXPECT(all.size() == size_t(Q) * dm && std::equal(row4.begin(), row4.end(), all.begin() + 4 * dm));
+  }
+  // ---- audits (audit.hpp:37-49) ----
+  {
+    AuditOptions ao;
+    ao.min_queries = 300;
+    auto a = run_regime_equivalence_audit(ao);
+    if (!a.passed()) std::printf("regime audit: seed %llu row %u %s\n", (unsigned long long)a.failure.instance_seed, a.failure.query_row, a.failure.detail.c_str());
+    EXPECT(a.passed() && a.queries_checked >= 300 && a.instances_run >= 1);
+    auto b = run_dense_regime_audit(ao);
+    if (!b.passed()) std::printf("dense audit: seed %llu row %u %s\n", (unsigned long long)b.failure.instance_seed, b.failure.query_row, b.failure.detail.c_str());
+    EXPECT(b.passed() && b.queries_checked >= 300);
+    auto c = run_subset_chain_audit(ao);
+    if (!c.passed()) std::printf("subset audit: seed %llu row %u %s\n", (unsigned long long)c.failure.instance_seed, c.failure.query_row, c.failure.detail.c_str());
+    EXPECT(c.passed() && c.queries_checked >= 300);
+    ao.inject_tie_mismatch = true;  // the failure path must fire
+    auto f = run_regime_equivalence_audit(ao);
+    EXPECT(!f.passed() && !f.failure.detail.empty());
+    AblationOptions ab;
+    ab.seq_len = 4096;
+    ab.token_budget = 512;
+    ab.seeds = 2;
+    ab.configs = {{64, 32, true}, {128, 16, true}, {128, 4, false}};
+    auto rows = run_overlap_ablation(ab);
+    EXPECT(rows.size() == 3);
+    for (const auto& r : rows) EXPECT(r.mean_overlap > 0.0 && r.mean_overlap <= 1.0 && r.min_overlap <= r.mean_overlap);
+    EXPECT(rows[0].mean_overlap > rows[2].mean_overlap);  // token refinement beats the block-sparse baseline
+    std::printf("ablation IoU vs flat: B=64,m=32 %.3f | B=128,m=16 %.3f | block-sparse B=128,m=4 %.3f\n", rows[0].mean_overlap,
+                rows[1].mean_overlap, rows[2].mean_overlap);
   }
   std::printf("%s: %d checks, %d failed\n", g_fail ? "FAILED" : "PASSED", g_run, g_fail);
   return g_fail ? 1 : 0;

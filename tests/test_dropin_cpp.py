@@ -27,7 +27,10 @@ def test_dropin_exports_reference_entry_points(built):
                 "hisa::IndexerInputs::IndexerInputs(", "hisa::make_random_inputs(", "hisa::load_tensor_file(",
                 "hisa::save_tensor_file(", "hisa::parallel_for(", "hisa::worker_count(", "hisa::analytic_cost(",
                 "hisa::run_bench(", "hisa::write_bench_csv(", "hisa::to_string(", "hisa::strategy_from_string(",
-                "hisa::gpu::Indexer::hisa_select_batch("]:
+                "hisa::gpu::Indexer::hisa_select_batch(", "hisa::sparse_attend(", "hisa::dense_attend(",
+                "hisa::AttentionInputs::AttentionInputs(", "hisa::run_regime_equivalence_audit(",
+                "hisa::run_dense_regime_audit(", "hisa::run_subset_chain_audit(", "hisa::run_overlap_ablation(",
+                "hisa::gpu::Attention::sparse_attend_batch("]:
         assert sym in out, f"{sym} not exported by libhisa_dropin.so"
 
 
