@@ -39,6 +39,9 @@ def parse_args():
     ap.add_argument("--token-budget", type=int, default=2048)
     ap.add_argument("--flat-steps", type=int, default=2, help="timed steps of the flat DSA comparison (0 = skip)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--attend-steps", type=int, default=2,
+                    help="timed runs of the downstream consumer (sparse_attend over the selected indices; 0 = skip)")
+    ap.add_argument("--d-model", type=int, default=128, help="latent width of the downstream consumer")
     ap.add_argument("--cpu-rows", type=int, default=768, help="rows of the workload the CPU baseline is timed on")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
@@ -374,6 +377,39 @@ def run_b200(a, rank, world, local_rank):
                 "scorer_ms": fk_ms, "top_k_ms": fstages["top_k_ms"] / max(fstages["calls"], 1),
                 "scorer_tflops": 2.0 * d * H * prefix / (fk_ms * 1e-3) / 1e12 if fk_ms > 0 else None}
 
+    # ---- the step after the path: sparse_attend over the [Q, k] indices just selected.
+    # Shared-KV latents [L, d_model] bf16 (16 MiB at 64K x 128: L2-resident), one state vector per query.
+    consumer = None
+    if a.attend_steps > 0:
+        step_hisa()
+        ix.synchronize()
+        dm = a.d_model
+        g.manual_seed(a.seed + 5000)
+        lat = torch.randn((L, dm), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+        hs = torch.randn((nq, dm), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+        u = torch.empty((nq, dm), device=dev, dtype=torch.float32)
+        _check = capi._check
+        _check(capi.lib().hisa_cuda_attn_set_latents(ix._ctx, capi._ptr(lat.data_ptr()), L, dm, capi.DTYPE_BF16, 0), ix._ctx)
+        att_ms = []
+        for it in range(a.attend_steps + 1):
+            ix.sparse_attend_raw(hs.data_ptr(), capi.DTYPE_BF16, pos.data_ptr(), nq, out_idx.data_ptr(), k, out_count.data_ptr(),
+                                 u.data_ptr())
+            if it:
+                att_ms.append(ix.attn_last_ms())
+        a_ms = float(np.median(att_ms))
+        picked = int(out_count.to(torch.int64).sum().item())
+        gather_bytes = picked * dm * 2
+        hbm_bytes = picked * 4 + nq * (dm * 2 + dm * 4 + 8) + L * dm * 2
+        consumer = {"op": "sparse_attend (hisa/attention.hpp:48-56) over the selected indices", "d_model": dm, "ms": a_ms,
+                    "queries_per_s": nq / (a_ms * 1e-3), "selected_tokens": picked,
+                    "gather_gbs_l2_to_sm": gather_bytes / (a_ms * 1e-3) / 1e9,
+                    "hbm": {"bound": "hbm", "achieved": hbm_bytes / (a_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                            "frac": hbm_bytes / (a_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                            "work": "indices + query states read, outputs written, latent table once (the gather itself is "
+                                    "served by L2: see gather_gbs_l2_to_sm)"},
+                    "finite": bool(torch.isfinite(u).all().item())}
+        del lat, hs, u
+
     # ---- end to end through the C ABI with HOST buffers (pinned), copies inside the timed region
     e2e = None
     if a.e2e_steps > 0:
@@ -444,7 +480,7 @@ def run_b200(a, rank, world, local_rank):
                                    "indices all-gathered inside the step" if world > 1 else "single GPU"},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
             "roofline": roofline, "stage_rooflines": stage_rooflines, "cpu_baseline": cpu, "flat_dsa": flat,
-            "stages_ms_per_step": per_call,
+            "stages_ms_per_step": per_call, "consumer_sparse_attend": consumer,
             "scorer_stall_fraction_of_cta_time": stalls,
             "candidate_pairs_per_step": cand_sum_all,
         }

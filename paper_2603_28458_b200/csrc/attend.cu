@@ -28,7 +28,7 @@ namespace hisa_dev {
 namespace {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
-constexpr int kAttnWarps = 4;
+constexpr int kAttnWarps = 1;  // one warp per CTA: the row index comes from blockIdx, so the compiler knows every loop bound is warp-uniform
 
 template <int WORDS>
 __device__ __forceinline__ void load_words(const uint32_t* __restrict__ p, uint32_t (&w)[WORDS]) {
@@ -80,7 +80,7 @@ __device__ __forceinline__ float transposed_reduce(float (&v)[TB], uint32_t lane
 
 // EPL elements of the (padded) model dimension per lane, TB rows per batch.
 template <int EPL, int TB, bool BF16>
-__global__ void __launch_bounds__(kAttnWarps * 32, 4) sparse_attend_kernel(const AttendArgs a) {
+__global__ void __launch_bounds__(kAttnWarps * 32, 16) sparse_attend_kernel(const AttendArgs a) {
   constexpr int WORDS = BF16 ? EPL / 2 : EPL;
   constexpr int LPR = 32 / TB;  // lanes that end up holding the same row's logit
   const uint32_t lane = threadIdx.x & 31;
