@@ -717,10 +717,23 @@ int select_pipelined(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, co
     if (nblk_host) HISA_TRY(ensure(ctx, ctx->st_nblk[i], P * 4));
   }
   const uint64_t nslices = (Q + P - 1) / P;
+  // HISA_PIPE_TRACE=1: timed events around every copy and kernel span, printed as a per-slice timeline (ms from the
+  // start of the call) — a debugging aid for the overlap, never on in measurements
+  const bool trace = env_u32("HISA_PIPE_TRACE", 0) != 0;
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.push_back(e);
+  };
+  mark(ctx->stream);
   auto copy_in_slice = [&](uint64_t s) -> int {
     const int b = int(s & 1);
     const uint64_t q0 = s * P, nq = std::min<uint64_t>(P, Q - q0);
     if (s >= 2) CU_TRY(ctx, cudaStreamWaitEvent(ctx->in_stream, ctx->ev_in_free[b], 0));
+    mark(ctx->in_stream);
     if (q_host)
       CU_TRY(ctx, cudaMemcpyAsync(ctx->st_q[b].p, static_cast<const char*>(queries) + q0 * q_row, nq * q_row,
                                   cudaMemcpyHostToDevice, ctx->in_stream));
@@ -730,6 +743,7 @@ int select_pipelined(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, co
     if (p_host)
       CU_TRY(ctx, cudaMemcpyAsync(ctx->st_pos[b].p, positions + q0, nq * 4, cudaMemcpyHostToDevice, ctx->in_stream));
     CU_TRY(ctx, cudaEventRecord(ctx->ev_in_ready[b], ctx->in_stream));
+    mark(ctx->in_stream);
     return HISA_OK;
   };
   HISA_TRY(copy_in_slice(0));
@@ -747,10 +761,13 @@ int select_pipelined(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, co
     uint32_t* cand_s = !out_cand ? nullptr : cand_host ? ctx->st_cand[b].as<uint32_t>() : out_cand + q0;
     int32_t* blk_s = (strat == kDsa || !out_blocks) ? nullptr : blk_host ? ctx->st_blk[b].as<int32_t>() : out_blocks + q0 * S;
     uint32_t* nblk_s = (strat == kDsa || !out_nblocks) ? nullptr : nblk_host ? ctx->st_nblk[b].as<uint32_t>() : out_nblocks + q0;
+    mark(ctx->stream);
     HISA_TRY(select_core(ctx, strat, q_s, g_s, p_s, nq, check_finite, idx_s, cnt_s, blk_s, nblk_s, cand_s));
+    mark(ctx->stream);
     CU_TRY(ctx, cudaEventRecord(ctx->ev_in_free[b], ctx->stream));
     CU_TRY(ctx, cudaEventRecord(ctx->ev_out_ready[b], ctx->stream));
     CU_TRY(ctx, cudaStreamWaitEvent(ctx->out_stream, ctx->ev_out_ready[b], 0));
+    mark(ctx->out_stream);
     if (idx_host)
       CU_TRY(ctx, cudaMemcpyAsync(out_idx + q0 * out_width, idx_s, nq * out_width * 4, cudaMemcpyDeviceToHost, ctx->out_stream));
     if (cnt_host) CU_TRY(ctx, cudaMemcpyAsync(out_count + q0, cnt_s, nq * 4, cudaMemcpyDeviceToHost, ctx->out_stream));
@@ -758,9 +775,28 @@ int select_pipelined(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, co
     if (blk_host) CU_TRY(ctx, cudaMemcpyAsync(out_blocks + q0 * S, blk_s, nq * S * 4, cudaMemcpyDeviceToHost, ctx->out_stream));
     if (nblk_host) CU_TRY(ctx, cudaMemcpyAsync(out_nblocks + q0, nblk_s, nq * 4, cudaMemcpyDeviceToHost, ctx->out_stream));
     CU_TRY(ctx, cudaEventRecord(ctx->ev_out_free[b], ctx->out_stream));
+    mark(ctx->out_stream);
   }
   CU_TRY(ctx, cudaStreamSynchronize(ctx->out_stream));
   CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (trace) {
+    // event order: [0] call start, then per slice s: in-begin/in-end are pushed when slice s is copied (slice 0 first,
+    // slice s+1 before the kernels of slice s), kernels-begin/end and out-begin/end in loop order
+    std::vector<float> t(tev.size());
+    for (size_t i = 0; i < tev.size(); ++i) cudaEventElapsedTime(&t[i], tev[0], tev[i]);
+    std::vector<float> in_b(nslices), in_e(nslices), k_b(nslices), k_e(nslices), o_b(nslices), o_e(nslices);
+    size_t i = 1;
+    in_b[0] = t[i++]; in_e[0] = t[i++];
+    for (uint64_t s = 0; s < nslices; ++s) {
+      if (s + 1 < nslices) { in_b[s + 1] = t[i++]; in_e[s + 1] = t[i++]; }
+      k_b[s] = t[i++]; k_e[s] = t[i++]; o_b[s] = t[i++]; o_e[s] = t[i++];
+    }
+    fprintf(stderr, "slice   h2d[beg end]     kernels[beg end]   d2h[beg end]  (ms)\n");
+    for (uint64_t s = 0; s < nslices; ++s)
+      fprintf(stderr, "%5llu  %7.3f %7.3f   %7.3f %7.3f   %7.3f %7.3f\n", (unsigned long long)s, in_b[s], in_e[s], k_b[s], k_e[s],
+              o_b[s], o_e[s]);
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
+  }
   return HISA_OK;
 }
 
