@@ -359,6 +359,46 @@ struct AblationOptions {
 std::vector<AblationRow> run_overlap_ablation(const AblationOptions& options);
 
 // ---------------------------------------------------------------------------------------------------
+// needle-in-a-haystack harness — reference: hisa/niah.hpp:14-86 (a caller of the path: every selection inside is a
+// device call; the haystack scores that place the needle "strictly above every haystack score" also come from the
+// device scorer)
+// ---------------------------------------------------------------------------------------------------
+struct NiahInstance {
+  IndexerInputs inputs;
+  std::vector<uint32_t> needle_positions;
+  uint64_t haystack_seed = 0;
+};
+NiahInstance generate_niah(uint32_t seq_len, double depth_fraction, uint64_t seed, const HisaConfig& cfg,
+                           double needle_sigmas = 6.0);
+double selection_overlap(const SelectionResult& a, const SelectionResult& b);  // IoU; BothEmpty if both are empty
+double needle_recall(const NiahInstance& instance, const SelectionResult& selection);
+struct NiahRecord {
+  Strategy strategy = Strategy::Dsa;
+  uint32_t seq_len = 0;
+  double depth = 0.0;
+  uint32_t seed_index = 0;
+  double recall = 0.0;
+  double overlap_vs_dsa = 0.0;
+};
+struct NiahGridParams {
+  std::vector<uint32_t> lengths = {1024, 2048, 4096, 8192, 16384, 32768};
+  std::vector<double> depths = {0.0, 0.25, 0.5, 0.75, 1.0};
+  uint32_t seeds = 100;
+  uint64_t base_seed = 42;
+  uint32_t block_size = 128;
+  uint32_t token_budget = 2048;
+  uint32_t num_heads = 4;
+  uint32_t dim = 16;
+  uint32_t ratio = 4;
+  double needle_sigmas = 6.0;
+  uint32_t threads = 0;  // accepted for source compatibility; the device batches instead
+  std::vector<Strategy> strategies = {Strategy::Dsa, Strategy::Hisa, Strategy::BlockSparse};
+};
+std::vector<NiahRecord> run_niah_grid(const NiahGridParams& params);
+void write_niah_csv(std::ostream& os, const std::vector<NiahRecord>& records);
+void write_niah_grid_dat(std::ostream& os, const std::vector<NiahRecord>& records, Strategy strategy);
+
+// ---------------------------------------------------------------------------------------------------
 // batched device entry points (new; a per-row device call is meaningless at scale)
 // ---------------------------------------------------------------------------------------------------
 namespace gpu {

@@ -13,6 +13,7 @@
 #include "hisa/block_sparse.hpp"
 #include "hisa/bench.hpp"
 #include "hisa/hisa.hpp"
+#include "hisa/niah.hpp"
 #include "hisa/synth.hpp"
 #include "hisa/tensor_io.hpp"
 
@@ -310,6 +311,50 @@ int main() {
     EXPECT(rows[0].mean_overlap > rows[2].mean_overlap);  // token refinement beats the block-sparse baseline
     std::printf("ablation IoU vs flat: B=64,m=32 %.3f | B=128,m=16 %.3f | block-sparse B=128,m=4 %.3f\n", rows[0].mean_overlap,
                 rows[1].mean_overlap, rows[2].mean_overlap);
+  }
+  // ---- needle-in-a-haystack harness (niah.hpp) ----
+  {
+    const HisaConfig cfg(128, 16, 2048, 4, 16);
+    auto first = generate_niah(4096, 0.0, 11, cfg), last = generate_niah(4096, 1.0, 11, cfg), mid = generate_niah(4096, 0.5, 12, cfg);
+    EXPECT(first.needle_positions == std::vector<uint32_t>{0} && last.needle_positions == std::vector<uint32_t>{4095});
+    EXPECT(mid.needle_positions == std::vector<uint32_t>{2047} && mid.inputs.num_queries() == 1 && mid.inputs.position(0) == 4095);
+    auto flat = dsa_select(mid.inputs, cfg, 0);
+    EXPECT(needle_recall(mid, flat) == 1.0);  // the flat scan retrieves the needle by construction
+    {  // the needle is the single best-scoring token
+      std::vector<uint32_t> all(4096);
+      std::iota(all.begin(), all.end(), 0u);
+      auto sv = score_tokens(mid.inputs, 0, all);
+      EXPECT(std::max_element(sv.scores.begin(), sv.scores.end()) - sv.scores.begin() == 2047);
+    }
+    SelectionResult a{{0, 1, 2, 3}, {}, 0}, b{{2, 3, 4, 5}, {}, 0}, c{{7, 8}, {}, 0}, e{};
+    EXPECT(selection_overlap(a, a) == 1.0 && selection_overlap(a, c) == 0.0 && std::abs(selection_overlap(a, b) - 2.0 / 6.0) < 1e-15);
+    EXPECT(selection_overlap(a, b) == selection_overlap(b, a) && selection_overlap(a, e) == 0.0);
+    EXPECT(throws<BothEmpty>([&] { selection_overlap(e, e); }));
+    NiahGridParams gp;
+    gp.lengths = {1024, 8192, 16384};
+    gp.seeds = 6;
+    auto recs = run_niah_grid(gp);
+    EXPECT(recs.size() == 3u * 5u * 6u * 3u);
+    EXPECT(recs[0].strategy == Strategy::Dsa && recs[1].strategy == Strategy::Hisa && recs[2].strategy == Strategy::BlockSparse &&
+           recs[0].seq_len == 1024 && recs[3].seed_index == 1 && recs.back().seq_len == 16384 && recs.back().depth == 1.0);
+    double mean[3] = {0, 0, 0};
+    for (const auto& r : recs) mean[int(r.strategy)] += r.recall;
+    for (double& v : mean) v /= double(recs.size() / 3);
+    std::printf("NIAH mean recall: dsa %.3f  hisa %.3f  block-sparse %.3f\n", mean[0], mean[1], mean[2]);
+    EXPECT(mean[0] == 1.0);                       // DSA recall = 1 by construction
+    EXPECT(mean[1] >= mean[2] && mean[1] >= 0.9);  // HISA >= block-sparse in aggregate
+    for (const auto& r : recs) EXPECT(r.strategy != Strategy::Dsa || r.overlap_vs_dsa == 1.0);
+    auto again = run_niah_grid(gp);
+    bool same = again.size() == recs.size();
+    for (size_t i = 0; same && i < recs.size(); ++i) same = again[i].recall == recs[i].recall && again[i].overlap_vs_dsa == recs[i].overlap_vs_dsa;
+    EXPECT(same);                                 // deterministic for a given base seed
+    std::ostringstream csv, dat;
+    write_niah_csv(csv, recs);
+    write_niah_grid_dat(dat, recs, Strategy::Hisa);
+    const std::string csv_s = csv.str(), dat_s = dat.str();
+    EXPECT(csv_s.rfind("strategy,L,depth,seed,recall,overlap_vs_dsa\n", 0) == 0);
+    EXPECT(size_t(std::count(csv_s.begin(), csv_s.end(), '\n')) == recs.size() + 1);
+    EXPECT(dat_s.rfind("depth 1024 8192 16384\n", 0) == 0 && std::count(dat_s.begin(), dat_s.end(), '\n') == 6);
   }
   std::printf("%s: %d checks, %d failed\n", g_fail ? "FAILED" : "PASSED", g_run, g_fail);
   return g_fail ? 1 : 0;

@@ -30,7 +30,8 @@ def test_dropin_exports_reference_entry_points(built):
                 "hisa::gpu::Indexer::hisa_select_batch(", "hisa::sparse_attend(", "hisa::dense_attend(",
                 "hisa::AttentionInputs::AttentionInputs(", "hisa::run_regime_equivalence_audit(",
                 "hisa::run_dense_regime_audit(", "hisa::run_subset_chain_audit(", "hisa::run_overlap_ablation(",
-                "hisa::gpu::Attention::sparse_attend_batch("]:
+                "hisa::gpu::Attention::sparse_attend_batch(", "hisa::generate_niah(", "hisa::selection_overlap(",
+                "hisa::needle_recall(", "hisa::run_niah_grid(", "hisa::write_niah_csv(", "hisa::write_niah_grid_dat("]:
         assert sym in out, f"{sym} not exported by libhisa_dropin.so"
 
 
