@@ -7,12 +7,13 @@
 // |T_t| * d_model gathered elements. It is bound by the L2 -> SM gather (the latent table, 16 MiB at L = 64K and
 // d_model = 128 in bf16, stays L2-resident), not by the tensor pipe; the kernel is plain SIMT and organised around
 // that gather:
-//   * one warp per query row; lane l owns elements [l*EPL, (l+1)*EPL) of the model dimension, so a latent row is one
-//     fully coalesced warp load (256 B for d_model = 128 in bf16);
+//   * one warp per query row; R lanes share a latent row and each loads 16 bytes of it (R = 16 for d_model = 128 in
+//     bf16), so one warp-wide load instruction fetches 32 / R whole rows, fully coalesced;
 //   * TB rows are loaded back to back and kept in registers (TB x row-slice = 64 fp32 registers): TB independent loads in
 //     flight per warp, and each gathered byte crosses L2 -> SM once although it is used twice (logit, then weighted sum);
-//   * the TB partial dot products are combined with a transposed butterfly (31 shuffles for 32 rows instead of 160):
-//     afterwards lane j holds the logit of row j, so the exponentials are evaluated one per lane;
+//   * the TB partial dot products of a lane are combined with a transposed butterfly inside the R-lane group (TB - 1
+//     shuffles per batch instead of TB * log2 R): afterwards every lane holds the logit of one row, so the
+//     exponentials are evaluated one per lane; padding entries load row 0 unpredicated and are masked in the softmax;
 //   * online softmax across batches (running maximum, rescaled accumulators), fp32 throughout.
 // The optional weights output first receives the logits and is normalised by the same lanes at the end.
 #include <cuda_bf16.h>
@@ -54,12 +55,13 @@ __device__ __forceinline__ float elem(const uint32_t* w, int e) {
   else return __uint_as_float(w[e]);
 }
 
-// v[i] holds this lane's partial sum for row i; returns the full sum of row (lane / (32 / TB)).
-template <int TB>
+// v[i] holds this lane's partial sum for row slot i, over the R lanes (a contiguous, R-aligned lane group) that share
+// the slot's row; returns the full sum of slot (lane % R) / (R / TB). TB <= R, both powers of two.
+template <int TB, int R>
 __device__ __forceinline__ float transposed_reduce(float (&v)[TB], uint32_t lane) {
   int n = TB;
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
+  for (int o = R / 2; o >= 1; o >>= 1) {
     if (n > 1) {
       n >>= 1;
       const bool up = (lane & o) != 0;
@@ -78,12 +80,19 @@ __device__ __forceinline__ float transposed_reduce(float (&v)[TB], uint32_t lane
   return v[0];
 }
 
-// EPL elements of the (padded) model dimension per lane, TB rows per batch.
-template <int EPL, int TB, bool BF16>
+// R lanes share a latent row, EPL elements of the (padded) model dimension per lane: dm_pad = R * EPL. A warp-wide
+// load instruction ("slot") therefore fetches 32 / R rows; TB slots form a batch.
+template <int EPL, int R, bool BF16>
 __global__ void __launch_bounds__(kAttnWarps * 32, 16) sparse_attend_kernel(const AttendArgs a) {
   constexpr int WORDS = BF16 ? EPL / 2 : EPL;
-  constexpr int LPR = 32 / TB;  // lanes that end up holding the same row's logit
+  constexpr int RPS = 32 / R;                                   // rows per slot
+  constexpr int TB0 = EPL <= 2 ? 32 : 64 / EPL;                 // TB x EPL = 64 fp32 values per lane
+  constexpr int TB = TB0 < 32 / RPS ? TB0 : 32 / RPS;           // a batch holds at most 32 rows (one index per lane)
+  constexpr int ROWS = TB * RPS;                                // rows per batch
+  constexpr int LPR = R / TB;                                   // lanes that end up holding the same row's logit
+  static_assert(TB <= R && LPR >= 1, "transposed_reduce needs TB <= R");
   const uint32_t lane = threadIdx.x & 31;
+  const uint32_t sub = lane / R, rl = lane % R;                 // which row of a slot, which slice of the row
   const uint32_t w = blockIdx.x * kAttnWarps + (threadIdx.x >> 5);
   if (w >= a.num_rows) return;
   // dense mode: rows differ in length by orders of magnitude; hand out the long ones first
@@ -94,12 +103,13 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 16) sparse_attend_kernel(cons
                            : (bad_pos ? 0u : t + 1u);
   const int32_t* idx = a.idx ? a.idx + uint64_t(row) * a.idx_stride : nullptr;
   float* wout = a.weights ? a.weights + uint64_t(row) * a.weights_stride : nullptr;
-  const uint32_t* lat = static_cast<const uint32_t*>(a.latents);
-  const uint32_t row_words = a.dm_pad / (BF16 ? 2 : 1);
+  // byte arithmetic: row address = lane base + token * row bytes is ONE 32x32+64 multiply-add per load
+  const char* lane_base = static_cast<const char*>(a.latents) + rl * (WORDS * 4);
+  const uint32_t row_bytes = a.dm_pad * (BF16 ? 2u : 4u);
 
   float q[EPL];
 #pragma unroll
-  for (int e = 0; e < EPL; ++e) q[e] = a.queries[uint64_t(row) * a.dm_pad + lane * EPL + e];
+  for (int e = 0; e < EPL; ++e) q[e] = a.queries[uint64_t(row) * a.dm_pad + rl * EPL + e];
 
   float acc[EPL];
 #pragma unroll
@@ -107,24 +117,23 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 16) sparse_attend_kernel(cons
   float m = -CUDART_INF_F, l = 0.f;
   uint32_t flags = bad_pos ? 4u : 0u;
   const float scale2 = a.scale * 1.4426950408889634f;  // logits in base 2
+  const uint32_t mine = (rl / LPR) * RPS + sub;          // row of the batch whose logit this lane ends up holding
 
-  for (uint32_t b0 = 0; b0 < n; b0 += TB) {
+  for (uint32_t b0 = 0; b0 < n; b0 += ROWS) {
     int32_t my_tok = -1;
-    if (lane < TB && b0 + lane < n) my_tok = idx ? idx[b0 + lane] : int32_t(b0 + lane);
+    if (lane < ROWS && b0 + lane < n) my_tok = idx ? idx[b0 + lane] : int32_t(b0 + lane);
     if (my_tok >= 0 && (uint32_t(my_tok) > t || uint32_t(my_tok) >= a.seq_len)) {
       flags |= 2u;  // CausalViolation (attention.hpp:52)
       my_tok = -1;
     }
+    // padding and rejected entries load row 0 (always there) and are masked out of the softmax below: the loads of
+    // a batch carry no predicates
+    const uint32_t load_tok = uint32_t(max(my_tok, 0));
     uint32_t raw[TB][WORDS];
 #pragma unroll
     for (int i = 0; i < TB; ++i) {
-      const int32_t tok = __shfl_sync(kFull, my_tok, i);
-      if (tok >= 0) {
-        load_words<WORDS>(lat + uint64_t(tok) * row_words + lane * WORDS, raw[i]);
-      } else {
-#pragma unroll
-        for (int x = 0; x < WORDS; ++x) raw[i][x] = 0u;
-      }
+      const uint32_t tok = __shfl_sync(kFull, load_tok, i * RPS + sub);
+      load_words<WORDS>(reinterpret_cast<const uint32_t*>(lane_base + uint64_t(tok) * row_bytes), raw[i]);
     }
     float part[TB];
 #pragma unroll
@@ -134,11 +143,10 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 16) sparse_attend_kernel(cons
       for (int e = 0; e < EPL; ++e) s = fmaf(q[e], elem<BF16>(raw[i], e), s);
       part[i] = s;
     }
-    const float dot = transposed_reduce<TB>(part, lane);
-    const uint32_t mine = lane / LPR;  // row of the batch whose logit this lane holds
+    const float dot = transposed_reduce<TB, R>(part, lane);
     const bool valid = __shfl_sync(kFull, my_tok, mine) >= 0;
     const float x = valid ? dot * scale2 : -CUDART_INF_F;
-    if (wout && (lane % LPR) == 0 && b0 + mine < n) wout[b0 + mine] = x;
+    if (wout && (rl % LPR) == 0 && b0 + mine < n) wout[b0 + mine] = x;
     float bm = x;
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(kFull, bm, o));
@@ -154,27 +162,33 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 16) sparse_attend_kernel(cons
     for (int e = 0; e < EPL; ++e) acc[e] *= corr;
 #pragma unroll
     for (int i = 0; i < TB; ++i) {
-      const float pi = __shfl_sync(kFull, p, i * LPR);
+      const float pi = __shfl_sync(kFull, p, sub * R + i * LPR);  // the lane of this row group that holds slot i
 #pragma unroll
       for (int e = 0; e < EPL; ++e) acc[e] = fmaf(pi, elem<BF16>(raw[i], e), acc[e]);
     }
   }
-  // every row's weight was counted by its LPR lanes
+  // every row's weight was counted by its LPR lanes; the RPS row groups hold partial outputs of disjoint rows
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) l += __shfl_xor_sync(kFull, l, o);
   l *= 1.f / float(LPR);
+#pragma unroll
+  for (int o = R; o < 32; o <<= 1)
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[e] += __shfl_xor_sync(kFull, acc[e], o);
   if (!(l > 0.f)) flags |= 1u;  // EmptySelection (attention.hpp:51): nothing to normalise over
   const float inv = l > 0.f ? 1.f / l : 0.f;
+  if (sub == 0) {
 #pragma unroll
-  for (int e = 0; e < EPL; ++e) {
-    const uint32_t c = lane * EPL + e;
-    if (c < a.d_model) a.out[uint64_t(row) * a.d_model + c] = acc[e] * inv;
+    for (int e = 0; e < EPL; ++e) {
+      const uint32_t c = rl * EPL + e;
+      if (c < a.d_model) a.out[uint64_t(row) * a.d_model + c] = acc[e] * inv;
+    }
   }
   if (wout) {
     // the lane that stored a logit turns it into the weight (same thread: no fence needed)
-    for (uint32_t b0 = 0; b0 < a.weights_stride; b0 += TB) {
-      const uint32_t j = b0 + lane / LPR;
-      if ((lane % LPR) == 0 && j < a.weights_stride) wout[j] = (j < n && l > 0.f) ? exp2f(wout[j] - m) * inv : 0.f;
+    for (uint32_t b0 = 0; b0 < a.weights_stride; b0 += ROWS) {
+      const uint32_t j = b0 + mine;
+      if ((rl % LPR) == 0 && j < a.weights_stride) wout[j] = (j < n && l > 0.f) ? exp2f(wout[j] - m) * inv : 0.f;
     }
   }
   const uint32_t report = lane == 0 ? flags : (flags & 2u);  // bits 0 and 2 are warp-uniform
@@ -199,12 +213,10 @@ __global__ void pad_rows_kernel(const Src* __restrict__ src, uint64_t rows, uint
   }
 }
 
-template <int EPL, bool BF16>
-int launch_attend_epl(const AttendArgs& a, cudaStream_t stream) {
-  // TB x EPL = 64 fp32 values per lane (the compiler widens bf16 slices once and keeps them for both uses)
-  constexpr int TB = EPL <= 2 ? 32 : 64 / EPL;
+template <int EPL, int R, bool BF16>
+int launch_attend_shape(const AttendArgs& a, cudaStream_t stream) {
   const uint32_t grid = (a.num_rows + kAttnWarps - 1) / kAttnWarps;
-  sparse_attend_kernel<EPL, TB, BF16><<<grid, kAttnWarps * 32, 0, stream>>>(a);
+  sparse_attend_kernel<EPL, R, BF16><<<grid, kAttnWarps * 32, 0, stream>>>(a);
   return 1;
 }
 
@@ -218,21 +230,21 @@ uint32_t attend_padded_dim(uint32_t d_model, bool bf16) {
 
 int launch_sparse_attend(const AttendArgs& a, cudaStream_t stream) {
   if (a.num_rows == 0) return 0;
-  const int epl = int(a.dm_pad / 32);
+  // a lane loads 16 bytes of a row where the row is long enough for that (8 bf16 / 4 f32 elements); R = lanes per row
   if (a.latents_bf16) {
-    switch (epl) {
-      case 2: return launch_attend_epl<2, true>(a, stream);
-      case 4: return launch_attend_epl<4, true>(a, stream);
-      case 8: return launch_attend_epl<8, true>(a, stream);
-      case 16: return launch_attend_epl<16, true>(a, stream);
+    switch (a.dm_pad) {
+      case 64: return launch_attend_shape<8, 8, true>(a, stream);
+      case 128: return launch_attend_shape<8, 16, true>(a, stream);
+      case 256: return launch_attend_shape<8, 32, true>(a, stream);
+      case 512: return launch_attend_shape<16, 32, true>(a, stream);
     }
   } else {
-    switch (epl) {
-      case 1: return launch_attend_epl<1, false>(a, stream);
-      case 2: return launch_attend_epl<2, false>(a, stream);
-      case 4: return launch_attend_epl<4, false>(a, stream);
-      case 8: return launch_attend_epl<8, false>(a, stream);
-      case 16: return launch_attend_epl<16, false>(a, stream);
+    switch (a.dm_pad) {
+      case 32: return launch_attend_shape<4, 8, false>(a, stream);
+      case 64: return launch_attend_shape<4, 16, false>(a, stream);
+      case 128: return launch_attend_shape<4, 32, false>(a, stream);
+      case 256: return launch_attend_shape<8, 32, false>(a, stream);
+      case 512: return launch_attend_shape<16, 32, false>(a, stream);
     }
   }
   return 0;
