@@ -32,7 +32,7 @@ for r in rows[hdr + 1:]:
 total = sum(v[1] for v in agg.values())
 with open(os.path.join(out, f"{tag}_launches_summary.txt"), "w") as f:
     f.write("ncu --metrics gpu__time_duration.sum --clock-control none : python bench.py --steps 2 --warmup 1 --flat-steps 1\n")
-    f.write("(5 hisa_select calls: 1 warm-up + 2 timed + 2 of the instrumented stall-statistics pass, whose scorer is the <..., 1> instantiation; 2 dsa_select calls; C3, L=Q=65536; times are cold-cache and serialised)\n\n")
+    f.write("(6 hisa_select calls: 1 warm-up + 2 timed + 2 of the instrumented stall-statistics pass, whose scorer is the <..., 1> instantiation, + 1 feeding the consumer; 2 dsa_select calls; 3 sparse_attend calls of the consumer leg; C3, L=Q=65536; times are cold-cache and serialised)\n\n")
     f.write(f"{'kernel':70s} {'launches':>8s} {'total ms':>10s} {'share':>7s}\n")
     for name in sorted(agg, key=lambda n: -agg[n][1]):
         f.write(f"{name[:70]:70s} {agg[name][0]:8d} {agg[name][1]:10.3f} {100 * agg[name][1] / total:6.1f}%\n")

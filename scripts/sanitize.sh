@@ -8,6 +8,8 @@ mkdir -p gpurun_out
 timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests -m gpu -q -x -p no:cacheprovider \
   -k "lattice_inputs_bit_exact and 1-shape1 or fp8_lattice or top_k_on_given_scores and 9000 or pool_append or decode_placement" \
   > gpurun_out/memcheck.log 2>&1; echo "memcheck rc=$?"; tail -3 gpurun_out/memcheck.log
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_attention.py -m gpu -q -x \
+  -p no:cacheprovider -k "not full_size" > gpurun_out/memcheck_attend.log 2>&1; echo "memcheck (consumer) rc=$?"; tail -3 gpurun_out/memcheck_attend.log
 timeout 1500 compute-sanitizer --tool racecheck --racecheck-report analysis python -m pytest tests -m gpu -q -x -p no:cacheprovider \
   -k "top_k_on_given_scores or select_blocks_on_given or eligible or spec_examples" > gpurun_out/racecheck.log 2>&1
 echo "racecheck rc=$?"; grep -E "RACECHECK SUMMARY|passed|failed" gpurun_out/racecheck.log
