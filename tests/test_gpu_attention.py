@@ -160,3 +160,40 @@ def test_full_size_k2048_rows_against_sampled_oracle(oracle):
     want = oracle.attend_batch(capi.bf16_bits_to_f32(qb), capi.bf16_bits_to_f32(lb), pos, sel[rows], np.full(rows.shape[0], k, np.uint32),
                                rows=rows, scale=0.05)
     assert np.abs(out[rows] - want).max() <= TOL
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("HISA_STRESS_SEEDS", "10"))))
+def test_random_shapes_against_oracle(oracle, seed):
+    """Seeded random (L, Q, d_model, k, storage, scale) with ragged selections: duplicates, unsorted order, counts from 1
+    to k, padding entries inside the counted range (skipped by both sides), query positions 0 and L - 1."""
+    rng = np.random.default_rng(7000 + seed)
+    dm = int(rng.choice([1, 3, 16, 31, 33, 64, 65, 96, 128, 129, 200, 256, 384, 512]))
+    L = int(rng.integers(1, 5000))
+    Q = int(rng.integers(1, 150))
+    k = int(rng.integers(1, 300))
+    bf16 = bool(rng.integers(0, 2))
+    scale = float(rng.choice([0.0, 0.01, 0.3]))
+    q_in, l_in, pos, q_f, l_f = _instance(8000 + seed, L, Q, dm, bf16)
+    pos[0], pos[-1] = 0, L - 1
+    pos.sort()
+    sel = np.full((Q, k), -1, np.int32)
+    cnt = np.zeros(Q, np.uint32)
+    for r in range(Q):
+        n = int(rng.integers(1, k + 1))
+        sel[r, :n] = rng.integers(0, int(pos[r]) + 1, n)          # duplicates and arbitrary order allowed
+        if n > 2 and rng.random() < 0.3:
+            sel[r, int(rng.integers(1, n))] = -1                   # a hole inside the counted range
+        cnt[r] = n
+    with _indexer() as ix:
+        ix.attn_set_latents(l_in)
+        out, w = ix.sparse_attend(q_in, pos, sel, cnt, scale=scale, want_weights=True)
+    # the oracle takes exact index lists: drop the holes, remember where the kept entries sat
+    want = np.zeros((Q, dm), np.float32)
+    ww = np.zeros((Q, k), np.float64)
+    for r in range(Q):
+        keep = np.flatnonzero(sel[r, :cnt[r]] >= 0)
+        o, wr = oracle.attend_batch(q_f, l_f, pos, sel[r:r + 1, keep], np.uint32([keep.size]), rows=np.uint32([r]), scale=scale,
+                                    want_weights=True)
+        want[r], ww[r, keep] = o[0], wr[0]
+    assert np.abs(out - want).max() <= TOL, (dm, L, Q, k, bf16)
+    assert np.abs(w - ww).max() <= TOL
