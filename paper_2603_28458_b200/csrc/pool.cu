@@ -6,6 +6,7 @@
 // incremental tail update run the same per-column sequential double accumulation, so they agree bit for
 // bit with each other and with a CPU loop in the same order.
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 #include <cuda_fp8.h>
 
@@ -204,6 +205,111 @@ pool_update_fp8_kernel(const uint8_t* __restrict__ key8, const float* __restrict
   for (uint32_t g = 0; g < nseg_p; ++g) pooled_op[b * (uint64_t(nseg_p) * kDim) + g * kDim + c] = parts[g];
 }
 
+// Batch build (north-star kernel 1): the same per-column, position-ordered double accumulation, fed from shared
+// memory. One CTA per block; the block's rows are contiguous in HBM, so they arrive as bulk copies (cp.async.bulk,
+// 64 rows = 16 KB per copy for bf16 storage, two copies in flight per CTA, ~4 CTAs per SM): the whole key array is
+// requested within the first microsecond and streams at DRAM speed, while the one-thread-per-column kernel above
+// fetched 256 bytes per warp-instruction with eight rows in flight (45 us for 16 MiB: 6 % of the HBM roofline). The
+// adds, their order and the rounding are unchanged, so the summaries stay bit-identical to the incremental update and
+// to the CPU loop. FP8: rows are 128 bytes; the per-key scales of a chunk are fetched with plain loads.
+constexpr int kPoolChunkRows = 64;
+
+template <bool FP8>
+__global__ void __launch_bounds__(kDim)
+pool_update_staged_kernel(const void* __restrict__ key_op, const float* __restrict__ key_scale, uint32_t nseg_k,
+                          uint64_t first, uint64_t n, uint32_t block_size, uint32_t pool_max, double* __restrict__ sums,
+                          uint32_t* __restrict__ counts, __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p) {
+  extern __shared__ __align__(128) unsigned char pool_smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ float s_scale[2][kPoolChunkRows];
+  const uint64_t b = first / block_size + blockIdx.x;
+  const uint32_t c = threadIdx.x;
+  const uint64_t blk_lo = b * block_size;
+  const uint64_t s_lo = first > blk_lo ? first : blk_lo;
+  const uint64_t blk_hi = blk_lo + block_size;
+  const uint64_t s_hi = (first + n) < blk_hi ? (first + n) : blk_hi;
+  const bool fresh = (s_lo == blk_lo);
+  double acc = fresh ? 0.0 : sums[b * kDim + c];
+  const uint32_t row_bytes = FP8 ? uint32_t(kDim) : nseg_k * uint32_t(kDim) * 2u;
+  const uint32_t buf_bytes = kPoolChunkRows * row_bytes;
+  const uint32_t nrows = uint32_t(s_hi - s_lo);
+  const uint32_t nchunks = (nrows + kPoolChunkRows - 1) / kPoolChunkRows;
+  if (c == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t ch) {
+    const uint32_t buf = ch & 1u;
+    const uint64_t r0 = s_lo + uint64_t(ch) * kPoolChunkRows;
+    const uint32_t nr = min(uint32_t(kPoolChunkRows), uint32_t(s_hi - r0));
+    mbar_arrive_expect_tx(&bar[buf], nr * row_bytes);
+    bulk_load_1d(pool_smem + buf * buf_bytes, static_cast<const unsigned char*>(key_op) + r0 * row_bytes, nr * row_bytes,
+                 &bar[buf]);
+  };
+  if (c == 0) {
+    issue(0);
+    if (nchunks > 1) issue(1);
+  }
+  for (uint32_t ch = 0; ch < nchunks; ++ch) {
+    const uint32_t buf = ch & 1u;
+    const uint64_t r0 = s_lo + uint64_t(ch) * kPoolChunkRows;
+    const uint32_t nr = min(uint32_t(kPoolChunkRows), uint32_t(s_hi - r0));
+    if (FP8) {
+      if (c < nr) s_scale[buf][c] = key_scale[r0 + c];
+      __syncthreads();
+    }
+    mbar_wait(&bar[buf], (ch >> 1) & 1u);
+    const unsigned char* rows = pool_smem + buf * buf_bytes;
+#pragma unroll 8
+    for (uint32_t i = 0; i < nr; ++i) {
+      double v;
+      if (FP8) {
+        v = double(e4m3_to_float(rows[i * kDim + c]) * s_scale[buf][i]);
+      } else {
+        const __nv_bfloat16* row = reinterpret_cast<const __nv_bfloat16*>(rows + i * row_bytes) + c;
+        v = 0.0;
+        for (uint32_t g = 0; g < nseg_k; ++g) v += double(__bfloat162float(row[g * kDim]));
+      }
+      if (pool_max) acc = (fresh && r0 + i == s_lo) ? v : (v > acc ? v : acc);
+      else acc += v;
+    }
+    __syncthreads();  // every thread is done with this buffer
+    if (c == 0 && ch + 2 < nchunks) issue(ch + 2);
+  }
+  sums[b * kDim + c] = acc;
+  const uint32_t cnt = uint32_t(s_hi - blk_lo);
+  if (c == 0) counts[b] = cnt;
+  const double p = pool_max ? acc : acc / double(cnt);
+  __nv_bfloat16 parts[kMaxSeg];
+  split_bf16(float(p), int(nseg_p), parts);
+  for (uint32_t g = 0; g < nseg_p; ++g) pooled_op[b * (uint64_t(nseg_p) * kDim) + g * kDim + c] = parts[g];
+}
+
+template <bool FP8>
+bool launch_pool_staged(const void* key_op, const float* key_scale, uint32_t nseg_k, uint64_t first, uint64_t n,
+                        uint32_t block_size, uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op,
+                        uint32_t nseg_p, cudaStream_t stream) {
+  // decode-sized appends stay on the direct kernel: nothing to stage for a handful of rows
+  if (n < 32 || reinterpret_cast<uintptr_t>(key_op) % 16 != 0) return false;
+  const uint32_t row_bytes = FP8 ? uint32_t(kDim) : nseg_k * uint32_t(kDim) * 2u;
+  const size_t smem = size_t(2) * kPoolChunkRows * row_bytes;
+  auto kern = pool_update_staged_kernel<FP8>;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    configured = smem;
+  }
+  const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
+  kern<<<uint32_t(b1 - b0 + 1), kDim, smem, stream>>>(key_op, key_scale, nseg_k, first, n, block_size, pool_max, sums, counts,
+                                                      pooled_op, nseg_p);
+  return true;
+}
+
 __global__ void fill_f32_kernel(float* __restrict__ dst, uint64_t n, float v) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) dst[i] = v;
@@ -264,6 +370,8 @@ int launch_pool_update(const __nv_bfloat16* key_op, uint32_t nseg_k, uint64_t fi
                        uint32_t /*dim*/, uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op,
                        uint32_t nseg_p, cudaStream_t stream) {
   if (n == 0) return 0;
+  if (launch_pool_staged<false>(key_op, nullptr, nseg_k, first, n, block_size, pool_max, sums, counts, pooled_op, nseg_p, stream))
+    return 1;
   const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
   pool_update_kernel<<<uint32_t(b1 - b0 + 1), kDim, 0, stream>>>(key_op, nseg_k, first, n, block_size, pool_max, sums,
                                                                  counts, pooled_op, nseg_p);
@@ -274,6 +382,8 @@ int launch_pool_update_fp8(const uint8_t* key8, const float* key_scale, uint64_t
                            uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op, uint32_t nseg_p,
                            cudaStream_t stream) {
   if (n == 0) return 0;
+  if (launch_pool_staged<true>(key8, key_scale, 1, first, n, block_size, pool_max, sums, counts, pooled_op, nseg_p, stream))
+    return 1;
   const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
   pool_update_fp8_kernel<<<uint32_t(b1 - b0 + 1), kDim, 0, stream>>>(key8, key_scale, first, n, block_size, pool_max, sums,
                                                                      counts, pooled_op, nseg_p);
