@@ -262,18 +262,36 @@ pool_update_staged_kernel(const void* __restrict__ key_op, const float* __restri
     }
     mbar_wait(&bar[buf], (ch >> 1) & 1u);
     const unsigned char* rows = pool_smem + buf * buf_bytes;
-#pragma unroll 8
-    for (uint32_t i = 0; i < nr; ++i) {
-      double v;
-      if (FP8) {
-        v = double(e4m3_to_float(rows[i * kDim + c]) * s_scale[buf][i]);
-      } else {
-        const __nv_bfloat16* row = reinterpret_cast<const __nv_bfloat16*>(rows + i * row_bytes) + c;
-        v = 0.0;
-        for (uint32_t g = 0; g < nseg_k; ++g) v += double(__bfloat162float(row[g * kDim]));
+    // eight rows are read and widened together (independent work), then added in position order (the dependent chain)
+    for (uint32_t i0 = 0; i0 < nr; i0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t i = min(i0 + j, nr - 1);  // rows past the chunk repeat the last one and are not added
+        if (FP8) {
+          v[j] = double(e4m3_to_float(rows[i * kDim + c]) * s_scale[buf][i]);
+        } else {
+          const __nv_bfloat16* row = reinterpret_cast<const __nv_bfloat16*>(rows + i * row_bytes) + c;
+          if (nseg_k == 1) {
+            v[j] = double(__bfloat162float(row[0]));
+          } else {
+            v[j] = 0.0;
+            for (uint32_t g = 0; g < nseg_k; ++g) v[j] += double(__bfloat162float(row[g * kDim]));
+          }
+        }
       }
-      if (pool_max) acc = (fresh && r0 + i == s_lo) ? v : (v > acc ? v : acc);
-      else acc += v;
+      if (!pool_max && i0 + 8 <= nr) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc += v[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (i0 + j < nr) {
+            if (pool_max) acc = (fresh && r0 + i0 + j == s_lo) ? v[j] : (v[j] > acc ? v[j] : acc);
+            else acc += v[j];
+          }
+        }
+      }
     }
     __syncthreads();  // every thread is done with this buffer
     if (c == 0 && ch + 2 < nchunks) issue(ch + 2);
