@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(kWarpSelThreads) select_warp_kernel(SelectArgs
   }
   const uint32_t lo = __reduce_min_sync(FULL, kmin), hi = __reduce_max_sync(FULL, kmax);
   uint32_t T = hi, kk = keep;
+  bool all_ties = false;  // the descent stopped early: every key equal to T is kept
   if (lo != hi) {
     const int top = 31 - __clz(lo ^ hi);
     uint32_t prefix = hi & ~((2u << top) - 1u);  // bits above `top` are common to all candidates
@@ -368,12 +369,22 @@ __global__ void __launch_bounds__(kWarpSelThreads) select_warp_kernel(SelectArgs
 #pragma unroll
       for (int j = 0; j < KPL; ++j) c += ((key[j] >> bit) == want) ? 1u : 0u;
       c = __reduce_add_sync(FULL, c);
-      if (c >= kk) prefix |= 1u << bit;
+      if (c == kk) {
+        // the keys under this prefix are exactly the ones still to take: the threshold is their minimum and the
+        // remaining bits need no descent (distinct scores reach this point after ~log2(n) + a few bits)
+        uint32_t m = 0xFFFFFFFFu;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j)
+          if ((key[j] >> bit) == want) m = min(m, key[j]);
+        prefix = __reduce_min_sync(FULL, m);
+        all_ties = true;
+        break;
+      }
+      if (c > kk) prefix |= 1u << bit;
       else kk -= c;
     }
     T = prefix;
   }
-  const uint32_t need = kk;  // ties (key == T) to take
   uint32_t cG = 0, cE = 0;
 #pragma unroll
   for (int j = 0; j < KPL; ++j) {
@@ -381,6 +392,7 @@ __global__ void __launch_bounds__(kWarpSelThreads) select_warp_kernel(SelectArgs
     cE += key[j] == T;
   }
   const uint32_t totG = __reduce_add_sync(FULL, cG), totE = __reduce_add_sync(FULL, cE);
+  const uint32_t need = all_ties ? totE : kk;  // ties (key == T) to take
   const uint32_t skip = a.tie_break ? totE - need : 0u;
   uint32_t add_first = 0, add_last = 0;
   if (forced) {
