@@ -633,3 +633,38 @@ def test_random_shapes_fp8_lattice_bit_exact(oracle, seed):
         f = ix.dsa_select(q8, prob.gates, pos)
     compare_selection(oracle, prob, "hisa", h, np.arange(Q), 0.0, require_exact=True)
     compare_selection(oracle, prob, "dsa", f, np.arange(Q), 0.0, require_exact=True)
+
+
+# ------------------------------------------------------------------------------------------ query-row sharding
+@pytest.mark.parametrize("strategy", ["hisa", "dsa"])
+def test_sharded_rows_equal_unsharded_bit_for_bit(oracle, strategy):
+    """Determinism check of the multi-GPU plan on one device: the rows every rank of a 4-GPU job would own (zig-zag
+    tiles, `sharding.rank_rows`) are selected separately — fresh context per "rank", keys uploaded again — and merged
+    through the gathered-buffer order; the result must equal the single-context selection of all rows bit for bit."""
+    from paper_2603_28458_b200 import sharding
+    L = Q = 3000
+    H, d, B, m, k, tile, world = 64, 128, 64, 6, 256, 128, 4
+    pos = np.arange(Q, dtype=np.uint32)
+    prob = oracle.make_inputs("random", 21, L, pos, H, d, block_size=B, block_budget=m, token_budget=k)
+    q, kk = round_problem_to_bf16(prob)
+    with indexer_for(prob) as ix:
+        ix.upload_keys(kk)
+        ix.pool_build()
+        full = ix._select(strategy, q, prob.gates, pos)
+    pad = sharding.padded_rows_per_rank(Q, world, tile)
+    gathered = np.full((world * pad, k), -1, np.int32)
+    counts = np.zeros(world * pad, np.uint32)
+    for r in range(world):
+        rows = sharding.rank_rows(Q, world, r, tile)
+        with indexer_for(prob) as ix:
+            ix.upload_keys(kk)
+            ix.pool_build()
+            part = ix._select(strategy, q[rows], prob.gates[rows], pos[rows])
+        gathered[r * pad:r * pad + len(rows)] = part["idx"]
+        counts[r * pad:r * pad + len(rows)] = part["count"]
+    order = sharding.gathered_row_order(Q, world, tile)
+    merged = np.empty((Q, k), np.int32)
+    merged[order[order >= 0]] = gathered[order >= 0]
+    mcount = np.empty(Q, np.uint32)
+    mcount[order[order >= 0]] = counts[order >= 0]
+    assert np.array_equal(merged, full["idx"]) and np.array_equal(mcount, full["count"])
