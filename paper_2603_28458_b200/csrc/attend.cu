@@ -24,6 +24,7 @@
 #include <algorithm>
 
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace hisa_dev {
 namespace {
@@ -195,6 +196,222 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 16) sparse_attend_kernel(cons
   if (report) atomicOr(a.flag, report);
 }
 
+// ---------------------------------------------------------------------------------------------------------------
+// Warp-level tensor-core formulation for bf16 latents (d_model padded to 64 / 128 / 256). The SIMT kernel above spends
+// ~22 warp-instructions per gathered row (8 FMA + 4 widenings + shuffles); here a batch of 16 gathered rows is staged
+// once in shared memory (cp.async, 16 bytes per lane, double-buffered) and used by two sets of mma.sync.m16n8k16:
+//   logits   D[16 rows x 8]  = C[16 rows x d] . Q[d x 8]         A = the tile (ldmatrix), B = the query
+//   output   U[d x 8]       += C^T[d x 16 rows] . P[16 rows x 8]  A = the tile transposed (ldmatrix.trans), B = weights
+// An MMA has eight N columns and one query needs one: columns 0..2 carry the exact three-term bf16 split of the fp32
+// operand (query state for the logits, softmax weight for the output) and the three result columns are added, so both
+// products keep fp32 accuracy (bf16 weights alone would cost 2^-9 relative, far above the 1e-5 tolerance).
+// Measured mma.sync rate on B200 (tools/hmma_rate_bench.cu): 550 TFLOP/s, i.e. the 16 MMAs a batch needs cost ~1 ms
+// over the whole C3 workload, well under the gather ceiling.
+// ---------------------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void cp_async_16(uint32_t smem_addr, const void* gptr) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Term `which` (0, 1, 2) of an exact three-term bf16 expansion x = t0 + t1 + t2 by TRUNCATION: t0 is the leading 8
+// significand bits of x, x - t0 is exact, and so on (8 + 8 + 8 = the 24 bits of an fp32 significand). Masks and two
+// subtractions instead of three round-to-nearest conversions; which >= 3 gives zero.
+__device__ __forceinline__ uint32_t pack_terms(float lo, float hi, uint32_t which) {
+  uint32_t a = __float_as_uint(lo), b = __float_as_uint(hi);
+  if (which >= 1) {
+    a = __float_as_uint(lo - __uint_as_float(a & 0xFFFF0000u));
+    b = __float_as_uint(hi - __uint_as_float(b & 0xFFFF0000u));
+  }
+  if (which >= 2) {
+    a = __float_as_uint(__uint_as_float(a) - __uint_as_float(a & 0xFFFF0000u));
+    b = __float_as_uint(__uint_as_float(b) - __uint_as_float(b & 0xFFFF0000u));
+  }
+  if (which >= 3) a = b = 0u;
+  return (a >> 16) | (b & 0xFFFF0000u);
+}
+
+constexpr int kMmaRows = 16;  // gathered rows per batch = the M (logits) / K (output) extent of one MMA
+
+template <int DM>  // padded model dimension: 64, 128 or 256
+__global__ void __launch_bounds__(32, DM <= 128 ? 24 : 12) sparse_attend_mma_kernel(const AttendArgs a) {
+  constexpr int KS = DM / 16;                   // k-steps of the logits = 16-dim output blocks
+  constexpr uint32_t ROW_BYTES = DM * 2 + 16;   // 16 bytes of padding: ldmatrix rows land in distinct banks
+  constexpr uint32_t TILE_BYTES = kMmaRows * ROW_BYTES;
+  constexpr int CPR = DM * 2 / 16;              // 16-byte chunks per row
+  constexpr int RPI = 32 / CPR;                 // rows covered by one warp-wide cp.async (DM = 256: 1, 128: 2, 64: 4)
+  // two batches resident: one being reduced, one in flight (a third stage costs 28 registers of ring bookkeeping and
+  // the occupancy that goes with them: 4.76 ms against 3.83)
+  __shared__ __align__(16) unsigned char tiles[2 * TILE_BYTES];
+  const uint32_t lane = threadIdx.x;
+  const uint32_t g = lane >> 2, t = lane & 3u;
+  const uint32_t w = blockIdx.x;
+  const uint32_t row = a.idx ? w : a.num_rows - 1 - w;
+  const uint32_t tq = a.pos[row];
+  const bool bad_pos = tq >= a.seq_len;
+  const uint32_t n = a.idx ? (a.count ? min(a.count[row], uint32_t(a.idx_stride)) : uint32_t(a.idx_stride))
+                           : (bad_pos ? 0u : tq + 1u);
+  const int32_t* idx = a.idx ? a.idx + uint64_t(row) * a.idx_stride : nullptr;
+  float* wout = a.weights ? a.weights + uint64_t(row) * a.weights_stride : nullptr;
+  const char* lat = static_cast<const char*>(a.latents);
+  const uint32_t tile0 = smem_u32(tiles);
+  uint32_t flags = bad_pos ? 4u : 0u;
+  const float scale2 = a.scale * 1.4426950408889634f;
+
+  // B operand of the logits: column n = g holds term g of the query state (n >= 3: zero)
+  uint32_t qb[KS][2];
+  {
+    const float* qrow = a.queries + uint64_t(row) * DM;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const float2 lo = *reinterpret_cast<const float2*>(qrow + ks * 16 + 2 * t);
+      const float2 hi = *reinterpret_cast<const float2*>(qrow + ks * 16 + 2 * t + 8);
+      qb[ks][0] = pack_terms(lo.x, lo.y, g);
+      qb[ks][1] = pack_terms(hi.x, hi.y, g);
+    }
+  }
+  // per-lane pieces of the ldmatrix addresses: matrix j = lane / 8, row r = lane % 8 inside it
+  const uint32_t lj = lane >> 3, lr = lane & 7u;
+  const uint32_t a_off = (lr + (lj & 1u) * 8u) * ROW_BYTES + (lj >> 1) * 16u;        // logits: rows 0-7 / 8-15, k 0-7 / 8-15
+  const uint32_t at_off = (lr + (lj >> 1) * 8u) * ROW_BYTES + (lj & 1u) * 16u;        // output: dims 0-7 / 8-15, rows 0-7 / 8-15
+  // cp.async role: chunk c of row r0 + i * RPI
+  const uint32_t cp_chunk = lane % CPR, cp_row = lane / CPR;
+
+  auto fetch = [&](uint32_t b0, uint32_t buf, int32_t& tok_out) {
+    int32_t my = -1;
+    if (lane < kMmaRows && b0 + lane < n) my = idx ? idx[b0 + lane] : int32_t(b0 + lane);
+    if (my >= 0 && (uint32_t(my) > tq || uint32_t(my) >= a.seq_len)) {
+      flags |= 2u;
+      my = -1;
+    }
+    tok_out = my;
+    const uint32_t load_tok = uint32_t(max(my, 0));  // padding reads row 0 and is masked in the softmax
+    const uint32_t base = tile0 + buf * TILE_BYTES + cp_chunk * 16u;
+#pragma unroll
+    for (int i = 0; i < kMmaRows / RPI; ++i) {
+      const uint32_t r = i * RPI + cp_row;
+      const uint32_t tok = __shfl_sync(kFull, load_tok, r);
+      cp_async_16(base + r * ROW_BYTES, lat + uint64_t(tok) * (DM * 2) + cp_chunk * 16u);
+    }
+    cp_async_commit();
+  };
+
+  float u[KS][4];
+#pragma unroll
+  for (int d = 0; d < KS; ++d)
+#pragma unroll
+    for (int x = 0; x < 4; ++x) u[d][x] = 0.f;
+  float m = -CUDART_INF_F, l = 0.f;
+  int32_t next_tok = -1;
+  if (n) fetch(0, 0, next_tok);
+  uint32_t buf = 0;
+  for (uint32_t b0 = 0; b0 < n; b0 += kMmaRows, buf ^= 1u) {
+    const int32_t my_tok = next_tok;
+    if (b0 + kMmaRows < n) {
+      fetch(b0 + kMmaRows, buf ^ 1u, next_tok);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    const uint32_t tile = tile0 + buf * TILE_BYTES;
+    // ---- logits of the 16 rows: columns 0..2 are the three query terms
+    float d4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      uint32_t af[4];
+      ldmatrix_x4(af, tile + a_off + ks * 32u);
+      mma_bf16_16816(d4, af, qb[ks][0], qb[ks][1]);
+    }
+    // lane (g, 0) holds columns 0, 1 of rows g and g + 8, lane (g, 1) column 2
+    float x_lo = d4[0] + d4[1] + __shfl_down_sync(kFull, d4[0], 1);
+    float x_hi = d4[2] + d4[3] + __shfl_down_sync(kFull, d4[2], 1);
+    x_lo = __shfl_sync(kFull, x_lo, lane & ~3u);
+    x_hi = __shfl_sync(kFull, x_hi, lane & ~3u);
+    const bool v_lo = __shfl_sync(kFull, my_tok, g) >= 0, v_hi = __shfl_sync(kFull, my_tok, g + 8) >= 0;
+    x_lo = v_lo ? x_lo * scale2 : -CUDART_INF_F;
+    x_hi = v_hi ? x_hi * scale2 : -CUDART_INF_F;
+    if (wout && t == 0) {
+      if (b0 + g < n) wout[b0 + g] = x_lo;
+      if (b0 + g + 8 < n) wout[b0 + g + 8] = x_hi;
+    }
+    float bm = fmaxf(x_lo, x_hi);
+#pragma unroll
+    for (int o = 4; o <= 16; o <<= 1) bm = fmaxf(bm, __shfl_xor_sync(kFull, bm, o));
+    const float m_new = fmaxf(m, bm);
+    float p_lo = 0.f, p_hi = 0.f;
+    if (m_new > -CUDART_INF_F) {
+      if (m_new != m) {  // warp-uniform: the running maximum settles after a few batches
+        const float corr = exp2f(m - m_new);
+        l *= corr;
+#pragma unroll
+        for (int d = 0; d < KS; ++d)
+#pragma unroll
+          for (int x = 0; x < 4; ++x) u[d][x] *= corr;
+      }
+      p_lo = v_lo ? exp2f(x_lo - m_new) : 0.f;
+      p_hi = v_hi ? exp2f(x_hi - m_new) : 0.f;
+    }
+    m = m_new;
+    l += p_lo + p_hi;  // every row is counted by the 4 lanes of its group
+    // ---- B operand of the output: B[k = row][n = g] = term g of that row's weight
+    const float w0 = __shfl_sync(kFull, p_lo, (2 * t) * 4), w1 = __shfl_sync(kFull, p_lo, (2 * t + 1) * 4);
+    const float w8 = __shfl_sync(kFull, p_hi, (2 * t) * 4), w9 = __shfl_sync(kFull, p_hi, (2 * t + 1) * 4);
+    const uint32_t pb0 = pack_terms(w0, w1, g), pb1 = pack_terms(w8, w9, g);
+#pragma unroll
+    for (int d = 0; d < KS; ++d) {
+      uint32_t af[4];
+      ldmatrix_x4_trans(af, tile + at_off + d * 32u);
+      mma_bf16_16816(u[d], af, pb0, pb1);
+    }
+    __syncwarp();  // the tile is free for the copy that the next iteration issues into it
+  }
+#pragma unroll
+  for (int o = 4; o <= 16; o <<= 1) l += __shfl_xor_sync(kFull, l, o);  // groups hold disjoint rows; lanes of a group agree
+  if (!(l > 0.f)) flags |= 1u;
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  // U[dim][0..2] -> out: lane (g, 0) has columns 0, 1 of dims g and g + 8 of every 16-dim block, lane (g, 1) column 2
+#pragma unroll
+  for (int d = 0; d < KS; ++d) {
+    const float o_lo = u[d][0] + u[d][1] + __shfl_down_sync(kFull, u[d][0], 1);
+    const float o_hi = u[d][2] + u[d][3] + __shfl_down_sync(kFull, u[d][2], 1);
+    if (t == 0) {
+      const uint32_t c0 = d * 16 + g, c1 = c0 + 8;
+      if (c0 < a.d_model) a.out[uint64_t(row) * a.d_model + c0] = o_lo * inv;
+      if (c1 < a.d_model) a.out[uint64_t(row) * a.d_model + c1] = o_hi * inv;
+    }
+  }
+  if (wout && t == 0) {
+    for (uint32_t b0 = 0; b0 < a.weights_stride; b0 += kMmaRows) {
+      const uint32_t j0 = b0 + g, j1 = b0 + g + 8;
+      if (j0 < a.weights_stride) wout[j0] = (j0 < n && l > 0.f) ? exp2f(wout[j0] - m) * inv : 0.f;
+      if (j1 < a.weights_stride) wout[j1] = (j1 < n && l > 0.f) ? exp2f(wout[j1] - m) * inv : 0.f;
+    }
+  }
+  const uint32_t report = lane == 0 ? flags : (flags & 2u);
+  if (report) atomicOr(a.flag, report);
+}
+
+template <int DM>
+int launch_attend_mma(const AttendArgs& a, cudaStream_t stream) {
+  sparse_attend_mma_kernel<DM><<<a.num_rows, 32, 0, stream>>>(a);
+  return 1;
+}
+
 // src [rows, dim] (f32 | bf16) -> dst [rows, dim_pad] (f32 | bf16), zero filled beyond dim
 template <typename Src, typename Dst>
 __global__ void pad_rows_kernel(const Src* __restrict__ src, uint64_t rows, uint32_t dim, uint32_t dim_pad,
@@ -231,6 +448,13 @@ uint32_t attend_padded_dim(uint32_t d_model, bool bf16) {
 int launch_sparse_attend(const AttendArgs& a, cudaStream_t stream) {
   if (a.num_rows == 0) return 0;
   // a lane loads 16 bytes of a row where the row is long enough for that (8 bf16 / 4 f32 elements); R = lanes per row
+  if (a.latents_bf16 && !a.force_simt) {
+    switch (a.dm_pad) {
+      case 64: return launch_attend_mma<64>(a, stream);
+      case 128: return launch_attend_mma<128>(a, stream);
+      case 256: return launch_attend_mma<256>(a, stream);
+    }
+  }
   if (a.latents_bf16) {
     switch (a.dm_pad) {
       case 64: return launch_attend_shape<8, 8, true>(a, stream);

@@ -1497,6 +1497,7 @@ static int attend_impl(hisa_cuda_ctx* ctx, const void* query_states, uint32_t q_
   a.weights = !weights || dense ? nullptr : (w_dev ? weights : ctx->attn_w.as<float>());
   a.weights_stride = sel_stride;
   a.flag = ctx->flag.as<uint32_t>();
+  a.force_simt = env_u32("HISA_ATTEND_SIMT", 0);
   if (!ctx->attn_beg) {
     CU_TRY(ctx, cudaEventCreate(&ctx->attn_beg));
     CU_TRY(ctx, cudaEventCreate(&ctx->attn_end));

@@ -130,6 +130,7 @@ struct AttendArgs {
   float* weights;         // optional [num_rows, weights_stride], selection order, zero beyond the row's count
   uint64_t weights_stride;
   uint32_t* flag;         // device word, OR of: 1 empty selection, 2 causal violation, 4 position >= seq_len
+  uint32_t force_simt;    // HISA_ATTEND_SIMT: keep bf16 latents on the SIMT kernel (cross-check of the MMA kernel)
 };
 
 // ---- launchers (each returns the number of kernels it launched) ---------------------------------

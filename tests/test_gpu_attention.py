@@ -197,3 +197,22 @@ def test_random_shapes_against_oracle(oracle, seed):
         want[r], ww[r, keep] = o[0], wr[0]
     assert np.abs(out - want).max() <= TOL, (dm, L, Q, k, bf16)
     assert np.abs(w - ww).max() <= TOL
+
+
+@pytest.mark.parametrize("dm", [64, 100, 128, 256])
+def test_bf16_simt_and_mma_kernels_agree_with_the_oracle(oracle, dm, monkeypatch):
+    """bf16 latents run on the warp-MMA kernel (d_model <= 256); HISA_ATTEND_SIMT=1 keeps them on the SIMT kernel. Both
+    must meet the oracle tolerance, weights included, and agree with each other well inside it."""
+    L, Q, k = 2500, 61, 150
+    q_in, l_in, pos, q_f, l_f = _instance(40 + dm, L, Q, dm, True)
+    sel, cnt = _random_selection(np.random.default_rng(41 + dm), pos, k)
+    res = {}
+    for simt in ("0", "1"):
+        monkeypatch.setenv("HISA_ATTEND_SIMT", simt)
+        with _indexer() as ix:
+            ix.attn_set_latents(l_in)
+            res[simt] = ix.sparse_attend(q_in, pos, sel, cnt, want_weights=True)
+    want, ww = oracle.attend_batch(q_f, l_f, pos, sel, cnt, want_weights=True)
+    for out, w in res.values():
+        assert np.abs(out - want).max() <= TOL and np.abs(w - ww).max() <= TOL
+    assert np.abs(res["0"][0] - res["1"][0]).max() <= 2e-6
