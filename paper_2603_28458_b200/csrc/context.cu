@@ -423,6 +423,17 @@ uint32_t dense_chunk_for(const hisa_cuda_ctx* ctx, uint64_t nq, uint32_t ntiles)
   return chunk;
 }
 
+// Queries per chunk of the block-major refinement (one work item per chunk and selected key block). 512 queries
+// amortise a key-tile load over ~16 groups at prefill sizes; a call with few rows (the paper's 1024-row tail, a
+// pipeline slice) would then leave the 148 persistent CTAs with a handful of long items each (6.9 per SM at 1024
+// rows: 0.205 ms for stage 2 against 0.163 ms with 128-query chunks), so the chunk is halved until a call has at
+// least eight chunks (never below 64 queries).
+uint32_t list_chunk_for(const hisa_cuda_ctx* ctx, uint64_t nq) {
+  uint32_t chunk = ctx->chunk_list;
+  while (chunk > 64 && (nq + chunk - 1) / chunk < 8) chunk /= 2;
+  return chunk;
+}
+
 // stage 1: J[q, b] for rows [0, nq) -> ctx->J with stride Mpad
 int run_score_blocks(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, uint64_t nq, uint32_t Mpad) {
   const uint32_t M = uint32_t(num_blocks_of(ctx));
@@ -611,15 +622,16 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
       } else {
         // ---- stage 2: block-major refinement over the selected blocks, then top-k (hisa.hpp:30-45) ----
         const uint32_t spb = (B + kTileRows - 1) / kTileRows;
-        const uint32_t nchunks = uint32_t((nq + ctx->chunk_list - 1) / ctx->chunk_list);
-        const uint64_t items_cap = uint64_t(nchunks) * std::min<uint64_t>(M, uint64_t(ctx->chunk_list) * S) * spb;
+        const uint32_t chunk_list = list_chunk_for(ctx, nq);
+        const uint32_t nchunks = uint32_t((nq + chunk_list - 1) / chunk_list);
+        const uint64_t items_cap = uint64_t(nchunks) * std::min<uint64_t>(M, uint64_t(chunk_list) * S) * spb;
         HISA_TRY(ensure(ctx, ctx->work, size_t(items_cap) * sizeof(WorkItem)));
-        HISA_TRY(ensure(ctx, ctx->pairs, size_t(nchunks) * ctx->chunk_list * S * sizeof(uint2)));
+        HISA_TRY(ensure(ctx, ctx->pairs, size_t(nchunks) * chunk_list * S * sizeof(uint2)));
         HISA_TRY(ensure(ctx, ctx->cand, size_t(nq) * cand_cols * 4));
         uint32_t* sc = ctx->scalars.as<uint32_t>();
         {
           StageTimer timer(ctx, kStInvert);
-          count_launches(ctx, launch_invert_selection(sel, nsel, S, uint32_t(nq), ctx->chunk_list, M, B, spb,
+          count_launches(ctx, launch_invert_selection(sel, nsel, S, uint32_t(nq), chunk_list, M, B, spb,
                                                       ctx->work.as<WorkItem>(), sc, sc + 1, ctx->pairs.as<uint2>(),
                                                       ctx->stream));
           HISA_TRY(check_launch(ctx, "invert selection"));
