@@ -43,6 +43,14 @@ def test_dropin_host_layer_has_no_cuda_dependency_of_its_own(built):
     assert "cudaMalloc" not in und and "cuLaunch" not in und
 
 
+def test_host_layer_without_a_gpu(built):
+    """cpp/test_host.cpp: value types, validation rules, the RNG stream against the reference-compiled golden values,
+    index arithmetic, metrics, HSB files, fan-out — everything in the C++ layer that is host code runs here on CPU."""
+    r = subprocess.run([os.path.join(built, "test_host")], capture_output=True, text=True, timeout=120)
+    print(r.stdout[-3000:], r.stderr[-2000:])
+    assert r.returncode == 0 and "PASSED" in r.stdout, r.stdout[-3000:]
+
+
 @pytest.mark.gpu
 def test_dropin_spec_examples_on_gpu(built):
     r = subprocess.run([os.path.join(built, "test_dropin")], capture_output=True, text=True, timeout=600)
