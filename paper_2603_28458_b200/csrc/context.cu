@@ -624,14 +624,20 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
         const uint32_t spb = (B + kTileRows - 1) / kTileRows;
         const uint32_t chunk_list = list_chunk_for(ctx, nq);
         const uint32_t nchunks = uint32_t((nq + chunk_list - 1) / chunk_list);
-        const uint64_t items_cap = uint64_t(nchunks) * std::min<uint64_t>(M, uint64_t(chunk_list) * S) * spb;
+        // small calls: no work item longer than 4 MMA groups, so that the lists of the forced blocks (every query of
+        // the chunk selects the sink and the local block) do not become one SM's tail (decode: longest CTA 61K cycles
+        // against a mean of 28K before the split)
+        const uint32_t split = nq <= 2048 ? env_u32("HISA_LIST_SPLIT", 4u * kGroupQ) : 0u;
+        const uint64_t pairs_chunk = uint64_t(chunk_list) * S;
+        const uint64_t items_cap =
+            uint64_t(nchunks) * (std::min<uint64_t>(M, pairs_chunk) + (split ? pairs_chunk / split : 0)) * spb;
         HISA_TRY(ensure(ctx, ctx->work, size_t(items_cap) * sizeof(WorkItem)));
         HISA_TRY(ensure(ctx, ctx->pairs, size_t(nchunks) * chunk_list * S * sizeof(uint2)));
         HISA_TRY(ensure(ctx, ctx->cand, size_t(nq) * cand_cols * 4));
         uint32_t* sc = ctx->scalars.as<uint32_t>();
         {
           StageTimer timer(ctx, kStInvert);
-          count_launches(ctx, launch_invert_selection(sel, nsel, S, uint32_t(nq), chunk_list, M, B, spb,
+          count_launches(ctx, launch_invert_selection(sel, nsel, S, uint32_t(nq), chunk_list, M, B, spb, split,
                                                       ctx->work.as<WorkItem>(), sc, sc + 1, ctx->pairs.as<uint2>(),
                                                       ctx->stream));
           HISA_TRY(check_launch(ctx, "invert selection"));

@@ -153,9 +153,10 @@ int launch_build_dense_work(const uint32_t* pos, uint32_t nq, uint32_t chunk, ui
                             uint32_t ntiles, WorkItem* work, uint32_t* work_count, uint32_t* work_cursor,
                             cudaStream_t stream);
 // list work: per chunk of queries, the per-block lists of (row, slot*B) pairs and one item per (block, seg)
+// `split`: most queries one work item may carry (0 = unlimited); longer per-block lists become several items
 int launch_invert_selection(const int32_t* sel, const uint32_t* nsel, uint32_t sel_stride, uint32_t nq,
                             uint32_t chunk, uint32_t num_blocks, uint32_t block_size, uint32_t segs_per_block,
-                            WorkItem* work, uint32_t* work_count, uint32_t* work_cursor, uint2* pairs,
+                            uint32_t split, WorkItem* work, uint32_t* work_count, uint32_t* work_cursor, uint2* pairs,
                             cudaStream_t stream);
 // block-sparse output: tokens of the selected blocks clipped to <= t_eff
 int launch_expand_blocks(const int32_t* sel, const uint32_t* nsel, uint32_t sel_stride, const uint32_t* pos,

@@ -1186,8 +1186,8 @@ constexpr int kInvThreads = 256;
 __global__ void __launch_bounds__(kInvThreads)
 invert_selection_kernel(const int32_t* __restrict__ sel, const uint32_t* __restrict__ nsel, uint32_t sel_stride,
                         uint32_t nq, uint32_t chunk, uint32_t num_blocks, uint32_t block_size,
-                        uint32_t segs_per_block, WorkItem* __restrict__ work, uint32_t* __restrict__ work_count,
-                        uint2* __restrict__ pairs) {
+                        uint32_t segs_per_block, uint32_t split, WorkItem* __restrict__ work,
+                        uint32_t* __restrict__ work_count, uint2* __restrict__ pairs) {
   extern __shared__ __align__(16) uint32_t smem_u[];
   uint32_t* cnt = smem_u;                  // [num_blocks]
   uint32_t* off = smem_u + num_blocks;     // [num_blocks]
@@ -1205,7 +1205,10 @@ invert_selection_kernel(const int32_t* __restrict__ sel, const uint32_t* __restr
   const uint32_t per = (num_blocks + kInvThreads - 1) / kInvThreads;
   const uint32_t b0 = min(num_blocks, tid * per), b1 = min(num_blocks, b0 + per);
   uint32_t lsum = 0, lne = 0;
-  for (uint32_t b = b0; b < b1; ++b) { lsum += cnt[b]; lne += cnt[b] != 0; }
+  // a block's query list becomes ceil(n / split) work items: the forced blocks (sink, local) are selected by EVERY query
+  // of the chunk, and in a call with few rows one such list is a large share of an SM's whole work (decode: 16 of the
+  // ~10 groups an SM gets on average), so the host caps the list length per item for small calls
+  for (uint32_t b = b0; b < b1; ++b) { lsum += cnt[b]; lne += cnt[b] ? (cnt[b] - 1) / split + 1 : 0u; }
   uint32_t tot_pairs, tot_ne;
   uint32_t pre = block_scan_excl<kInvThreads>(lsum, scratch, tot_pairs);
   uint32_t pne = block_scan_excl<kInvThreads>(lne, scratch, tot_ne);
@@ -1216,16 +1219,17 @@ invert_selection_kernel(const int32_t* __restrict__ sel, const uint32_t* __restr
   for (uint32_t b = b0; b < b1; ++b) {
     const uint32_t n = cnt[b];
     off[b] = pre;
-    if (n) {
+    for (uint32_t done = 0; done < n; done += split) {
       for (uint32_t j = 0; j < segs_per_block; ++j) {
         WorkItem w;
         w.tile = b * segs_per_block + j;
-        w.first = pair_base + pre;
-        w.count = n;
+        w.first = pair_base + pre + done;
+        w.count = min(split, n - done);
         w.reserved = 0;
         work[item_base + pne * segs_per_block + j] = w;
       }
       ++pne;
+      if (split >= n) break;  // split may be 2^32 - 1: do not let `done += split` wrap
     }
     pre += n;
   }
@@ -1324,8 +1328,8 @@ int launch_build_dense_work(const uint32_t* pos, uint32_t nq, uint32_t chunk, ui
 }
 
 int launch_invert_selection(const int32_t* sel, const uint32_t* nsel, uint32_t sel_stride, uint32_t nq, uint32_t chunk,
-                            uint32_t num_blocks, uint32_t block_size, uint32_t segs_per_block, WorkItem* work,
-                            uint32_t* work_count, uint32_t* work_cursor, uint2* pairs, cudaStream_t stream) {
+                            uint32_t num_blocks, uint32_t block_size, uint32_t segs_per_block, uint32_t split,
+                            WorkItem* work, uint32_t* work_count, uint32_t* work_cursor, uint2* pairs, cudaStream_t stream) {
   if (nq == 0) return 0;
   zero_two_kernel<<<1, 1, 0, stream>>>(work_count, work_cursor);
   const size_t smem = (size_t(num_blocks) * 2 + 64) * sizeof(uint32_t);
@@ -1333,7 +1337,8 @@ int launch_invert_selection(const int32_t* sel, const uint32_t* nsel, uint32_t s
     cudaFuncSetAttribute(invert_selection_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   const uint32_t nchunks = (nq + chunk - 1) / chunk;
   invert_selection_kernel<<<nchunks, kInvThreads, smem, stream>>>(sel, nsel, sel_stride, nq, chunk, num_blocks,
-                                                                  block_size, segs_per_block, work, work_count, pairs);
+                                                                  block_size, segs_per_block, split ? split : 0xFFFFFFFFu, work,
+                                                                  work_count, pairs);
   return 2;
 }
 
