@@ -624,10 +624,13 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
         const uint32_t spb = (B + kTileRows - 1) / kTileRows;
         const uint32_t chunk_list = list_chunk_for(ctx, nq);
         const uint32_t nchunks = uint32_t((nq + chunk_list - 1) / chunk_list);
-        // small calls: no work item longer than 4 MMA groups, so that the lists of the forced blocks (every query of
-        // the chunk selects the sink and the local block) do not become one SM's tail (decode: longest CTA 61K cycles
-        // against a mean of 28K before the split)
-        const uint32_t split = nq <= 2048 ? env_u32("HISA_LIST_SPLIT", 4u * kGroupQ) : 0u;
+        // Every query of a chunk selects the sink and the local block, so those two query lists are far longer than
+        // the rest (512 queries = 128 MMA groups at prefill sizes, and the local block's item is the LAST one of the
+        // work list: one CTA's tail). Long lists are cut into several items: at most 128 queries (32 groups) at
+        // prefill sizes (stage 2 7.44 -> 7.22 ms, CTA balance 0.975 -> 0.988; 64 costs more in tile reloads than it
+        // balances), at most 16 queries for calls of <= 2048 rows, where one forced-block list was a large share of an
+        // SM's whole work (decode: longest CTA 61K cycles against a mean of 28K before the split).
+        const uint32_t split = nq <= 2048 ? env_u32("HISA_LIST_SPLIT", 4u * kGroupQ) : env_u32("HISA_LIST_SPLIT_BIG", 128u);
         const uint64_t pairs_chunk = uint64_t(chunk_list) * S;
         const uint64_t items_cap =
             uint64_t(nchunks) * (std::min<uint64_t>(M, pairs_chunk) + (split ? pairs_chunk / split : 0)) * spb;
