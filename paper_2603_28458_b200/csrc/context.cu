@@ -71,7 +71,7 @@ struct hisa_cuda_ctx {
   bool attn_timed = false;
 
   // tuning
-  uint32_t chunk_dense = 256, chunk_list = 512;
+  uint32_t chunk_dense = 128, chunk_list = 512;
   uint64_t workspace_bytes = 4ull << 30;
 
   // instrumentation
@@ -414,7 +414,9 @@ int ensure_pool(hisa_cuda_ctx* ctx) {
   return hisa_cuda_pool_build(ctx);
 }
 
-// Queries per dense work item. The configured chunk amortises a tile load over many queries; calls with few rows
+// Queries per dense work item. The configured chunk (128: stage 1 at 64K has 4 pooled-key tiles, and with 256-query
+// chunks its 640 items were 4.3 per SM, i.e. a CTA balance of 0.86; 1280 items give 0.95 and 0.57 -> 0.51 ms) amortises
+// a tile load over many queries; calls with few rows
 // (decode batches, the paper's 1024-row tail) would then produce fewer items than there are SMs, so the chunk is
 // halved until every SM has about two items (never below two MMA groups).
 uint32_t dense_chunk_for(const hisa_cuda_ctx* ctx, uint64_t nq, uint32_t ntiles) {
@@ -988,7 +990,7 @@ int hisa_cuda_create(int device, const hisa_cuda_config* cfg, hisa_cuda_ctx** ou
     for (int i = 0; i < kMaxSeg; ++i) ctx->terms_blk[i] = ctx->terms_tok[i];
   }
   ctx->q_zero_copy = bf16 && cfg->num_heads == uint32_t(kHeads) && cfg->dim == uint32_t(kDim);
-  ctx->chunk_dense = std::max<uint32_t>(env_u32("HISA_CHUNK_DENSE", 256), 4);
+  ctx->chunk_dense = std::max<uint32_t>(env_u32("HISA_CHUNK_DENSE", 128), 4);
   ctx->chunk_list = std::max<uint32_t>(env_u32("HISA_CHUNK_LIST", 512), 4);
   ctx->workspace_bytes = uint64_t(std::max<uint32_t>(env_u32("HISA_WORKSPACE_MB", 4096), 16)) << 20;
   ctx->pipe_rows = env_u32("HISA_PIPE_ROWS", 4096);  // 0 disables the host-buffer pipeline
