@@ -332,7 +332,13 @@ def run_b200(a, rank, world, local_rank):
         except Exception:
             traffic = None
     if fp8:
-        peaks = dict(peaks, tflops=2.0 * peaks["tflops"], source=peaks["source"] + " x2 for e4m3 (nominal fp8 : bf16 ratio)")
+        # dense e4m3 peak measured with the protocol of MEASURED_PEAKS.json (scripts/measure_fp8_peak.py); else 2x bf16
+        fpath = os.path.join(ROOT, "profiles", "fp8_peak.json")
+        if os.path.exists(fpath):
+            peaks = dict(peaks, tflops=float(json.load(open(fpath))["fp8_tflops_sustained"]),
+                         source="measured (profiles/fp8_peak.json: torch._scaled_mm e4m3 8192^3, sustained)")
+        else:
+            peaks = dict(peaks, tflops=2.0 * peaks["tflops"], source=peaks["source"] + " x2 for e4m3 (nominal fp8 : bf16 ratio)")
     roofline = {"bound": "tensor", "kernel": "score_tc_kernel (stage-2 block-major refinement)",
                 "achieved": achieved, "peak": peaks["tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["tflops"], "traffic": traffic, "peak_source": peaks["source"],
