@@ -1,10 +1,11 @@
-// hisa/api.hpp — the C++ surface of the B200 indexer library.
+// hisa/api.hpp — stand-in for the reference's proj/core/include/hisa/*.hpp where that tree is not installed.
 //
-// These are the reference's own entry points for the indexer hot path (namespace hisa, same names, same
-// argument meaning, same error behaviour), so code written against proj/core/include/hisa/*.hpp compiles
-// and links against this library unchanged. Each declaration cites the reference header it mirrors. The
-// per-file headers of the reference (hisa/dsa.hpp, hisa/hisa.hpp, ...) exist here as one-line forwards to
-// this file.
+// The library is built AGAINST THE REFERENCE'S OWN HEADERS when they are present (cpp/Makefile puts
+// $(REF)/include ahead of this directory; tests/test_reference_headers.py checks that every translation unit
+// then compiles with no header of this directory except hisa_gpu.hpp / hisa_cuda.h). This file restates the
+// same declarations (namespace hisa, same names, argument meaning and error behaviour, each citing the
+// reference header it mirrors) so that the drop-in also builds on a machine that only has this repository,
+// e.g. the GPU box; the per-file names of the reference (hisa/dsa.hpp, hisa/hisa.hpp, ...) forward here.
 //
 // What runs where: every function that scores or selects runs on the GPU through the C ABI in
 // hisa_cuda.h (there is no CPU implementation of the hot path in this library). Plain containers,
@@ -17,6 +18,7 @@
 #include <filesystem>
 #include <functional>
 #include <iosfwd>
+#include <optional>
 #include <random>
 #include <span>
 #include <stdexcept>
@@ -134,10 +136,6 @@ class IndexerInputs {
 // ---------------------------------------------------------------------------------------------------
 // block summaries — reference: hisa/block_summary.hpp:23-59
 // ---------------------------------------------------------------------------------------------------
-class BlockSummaryCache;
-BlockSummaryCache build_block_summaries(std::span<const float> keys, uint32_t dim, uint32_t block_size,
-                                        PoolMode mode = PoolMode::Mean, OpCounter* counter = nullptr);
-
 class BlockSummaryCache {
  public:
   BlockSummaryCache(uint32_t block_size, uint32_t dim, PoolMode mode = PoolMode::Mean);
@@ -152,14 +150,14 @@ class BlockSummaryCache {
   std::vector<double> pooled(uint32_t block) const;
 
  private:
-  // the batch build fills the summaries from the device kernel's output
-  friend BlockSummaryCache build_block_summaries(std::span<const float>, uint32_t, uint32_t, PoolMode, OpCounter*);
   uint32_t block_size_, dim_;
   PoolMode mode_;
   uint32_t num_tokens_ = 0;
-  std::vector<double> summary_;
+  std::vector<double> summary_;  // [num_blocks, dim]: sums (Mean) or running max (Max)
   std::vector<uint32_t> counts_;
 };
+BlockSummaryCache build_block_summaries(std::span<const float> keys, uint32_t dim, uint32_t block_size,
+                                        PoolMode mode = PoolMode::Mean, OpCounter* counter = nullptr);
 
 // ---------------------------------------------------------------------------------------------------
 // the flat indexer — reference: hisa/dsa.hpp:13-32
@@ -294,9 +292,6 @@ class AttentionInputs {
   std::span<const float> query_state(uint32_t row) const { return {&query_states_[std::size_t(row) * d_model_], d_model_}; }
   std::span<const float> latent(uint32_t pos) const { return {&latent_states_[std::size_t(pos) * d_model_], d_model_}; }
   uint32_t position(uint32_t row) const { return query_positions_[row]; }
-  const std::vector<float>& query_states_raw() const { return query_states_; }
-  const std::vector<float>& latent_states_raw() const { return latent_states_; }
-  const std::vector<uint32_t>& positions_raw() const { return query_positions_; }
 
  private:
   std::vector<float> query_states_, latent_states_;
@@ -322,9 +317,8 @@ struct AuditFailure {
 struct AuditReport {
   uint32_t instances_run = 0;
   uint32_t queries_checked = 0;
-  bool failed = false;
-  AuditFailure failure;  // meaningful when failed
-  bool passed() const { return !failed; }
+  std::optional<AuditFailure> failure;
+  bool passed() const { return !failure.has_value(); }
 };
 struct AuditOptions {
   uint64_t base_seed = 1;
@@ -398,70 +392,7 @@ std::vector<NiahRecord> run_niah_grid(const NiahGridParams& params);
 void write_niah_csv(std::ostream& os, const std::vector<NiahRecord>& records);
 void write_niah_grid_dat(std::ostream& os, const std::vector<NiahRecord>& records, Strategy strategy);
 
-// ---------------------------------------------------------------------------------------------------
-// batched device entry points (new; a per-row device call is meaningless at scale)
-// ---------------------------------------------------------------------------------------------------
-namespace gpu {
-
-enum class Storage { F32 = 0, BF16 = 1 };  // how q/k are stored on the device (hisa_dtype)
-
-// RAII handle on one hisa_cuda_ctx: one GPU, one stream. Not thread-safe (one per host thread / GPU).
-class Indexer {
- public:
-  Indexer(const HisaConfig& cfg, Storage storage = Storage::F32, int device = 0);
-  ~Indexer();
-  Indexer(const Indexer&) = delete;
-  Indexer& operator=(const Indexer&) = delete;
-
-  // keys [L, dim] float32 on the host (rounded to bf16 on upload when Storage::BF16)
-  void set_keys(std::span<const float> keys);
-  void append_keys(std::span<const float> keys);  // decode: incremental tail-block update
-  uint32_t seq_len() const;
-  uint32_t num_blocks() const;
-  void read_summaries(std::vector<double>& sums, std::vector<uint32_t>& counts) const;
-
-  // all rows of `inputs` in one device call each; results in row order
-  std::vector<SelectionResult> hisa_select_batch(const IndexerInputs& inputs, OpCounter* counter = nullptr);
-  std::vector<SelectionResult> dsa_select_batch(const IndexerInputs& inputs, OpCounter* counter = nullptr);
-  std::vector<SelectionResult> block_sparse_select_batch(const IndexerInputs& inputs, OpCounter* counter = nullptr);
-  // stage outputs for all rows
-  std::vector<ScoreVector> score_blocks_batch(const IndexerInputs& inputs);
-  std::vector<ScoreVector> score_prefix_batch(const IndexerInputs& inputs);  // score_tokens over [0, t]
-
-  // device time (ms) of the last batched call, by stage; see hisa_cuda_stage_times
-  struct Times { float score_blocks_ms, select_blocks_ms, invert_ms, score_tokens_ms, top_k_ms, total_ms; };
-  void enable_timing(bool on);
-  Times last_times();
-
-  void* raw() const { return ctx_; }  // the underlying hisa_cuda_ctx*
-
- private:
-  void* ctx_ = nullptr;
-  HisaConfig cfg_;
-  Storage storage_;
-};
-
-// Batched consumer: latents live on the device; one call attends all rows of `attn` over their selections.
-class Attention {
- public:
-  explicit Attention(const AttentionInputs& attn, Storage storage = Storage::F32, int device = 0);
-  ~Attention();
-  Attention(const Attention&) = delete;
-  Attention& operator=(const Attention&) = delete;
-  // out [Q, d_model] row-major; selections[r] belongs to query row r. weights (optional): per row, selection order.
-  std::vector<float> sparse_attend_batch(const std::vector<SelectionResult>& selections,
-                                         std::vector<std::vector<double>>* weights_out = nullptr);
-  std::vector<float> sparse_attend_rows(std::span<const uint32_t> rows, const std::vector<std::span<const uint32_t>>& selected,
-                                        std::vector<std::vector<double>>* weights_out = nullptr);
-  std::vector<float> dense_attend_batch();
-  std::vector<float> dense_attend_rows(std::span<const uint32_t> rows);
-  float last_kernel_ms();
-
- private:
-  void* ctx_ = nullptr;
-  const AttentionInputs* attn_;
-  Storage storage_;
-};
-
-}  // namespace gpu
 }  // namespace hisa
+
+// batched device entry points (namespace hisa::gpu): this library's own additions, see hisa_gpu.hpp
+#include "hisa_gpu.hpp"

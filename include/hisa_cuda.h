@@ -4,7 +4,7 @@
  * only).  The reference has no FFI of its own; each entry point below names the reference C++ interface
  * it replaces, batched over all query rows because a per-row device call is meaningless:
  *
- *   hisa_cuda_upload_keys / _pool_build / _pool_append / _pool_read
+ *   hisa_cuda_upload_keys / _pool_build / _pool_append / _pool_read / _pool_set
  *        <- hisa::build_block_summaries, BlockSummaryCache::append / pooled / count
  *           (proj/core/include/hisa/block_summary.hpp:23-59)
  *   hisa_cuda_score_blocks       <- hisa::score_blocks      (hisa/hisa.hpp:16-21)
@@ -133,6 +133,14 @@ int hisa_cuda_upload_keys_scaled(hisa_cuda_ctx* ctx, const void* keys, const flo
                                  int check_finite);
 /* (Re)builds all block summaries of the current sequence: build_block_summaries. */
 int hisa_cuda_pool_build(hisa_cuda_ctx* ctx);
+/* Installs caller-provided block summaries instead of pooling the uploaded keys: the contents of a
+ * hisa::BlockSummaryCache (hisa/block_summary.hpp:16-18: per-block f64 sums [num_blocks, dim] and counts [num_blocks])
+ * that covers the first num_tokens positions. The snapshot may be SHORTER than the key sequence (the decode contract,
+ * block_summary.hpp:27-30: append, then select): a query's eligible blocks are [0, floor(t/B)] clipped to num_blocks
+ * (hisa/hisa.hpp:16-21), its forced local block is the last eligible one. Host or device pointers.
+ * hisa_cuda_upload_keys / _pool_build / _pool_append go back to summaries computed from the context's keys. */
+int hisa_cuda_pool_set(hisa_cuda_ctx* ctx, const double* sums, const uint32_t* counts, uint64_t num_blocks,
+                       uint64_t num_tokens);
 /* Appends n keys [n, key_dim] at positions seq_len.. and updates only the touched tail blocks
  * (BlockSummaryCache::append, n times, in position order). DimensionMismatch if key_dim != dim. */
 int hisa_cuda_pool_append(hisa_cuda_ctx* ctx, const void* keys, uint64_t n, uint32_t key_dim);
@@ -165,6 +173,18 @@ int hisa_cuda_block_sparse_select(hisa_cuda_ctx* ctx, const void* queries, const
                                   const uint32_t* positions, uint64_t num_queries, int check_finite,
                                   int32_t* out_idx, uint32_t* out_count, int32_t* out_blocks,
                                   uint32_t* out_nblocks);
+
+/* Output placement for row-sharded runs (one context per GPU, each selecting a subset of the rows of one logical
+ * [Q_total, token_budget] result; "callers may fan out queries across workers").
+ * While set, hisa_cuda_hisa_select / _dsa_select treat out_idx / out_count / out_cand as the FULL arrays: the result
+ * of the call's i-th query is stored at row out_rows[i] (device array of at least num_queries entries; NULL = row i).
+ * Every result row is ALSO stored, by the selection kernel itself, at the same row of num_replicas (<= 7) replica
+ * arrays replica_idx[r] / replica_count[r] (may be NULL) — device memory that may live on OTHER GPUs with peer access
+ * enabled, so that on an NVLink/NVSwitch box the top-k kernel performs the all-gather of the indices with its own
+ * stores and no collective, staging copy or permutation follows it. All pointers must be device memory.
+ * out_rows == NULL && num_replicas == 0 switches placement off. */
+int hisa_cuda_set_output_placement(hisa_cuda_ctx* ctx, const uint32_t* out_rows, int num_replicas,
+                                   int32_t* const* replica_idx, uint32_t* const* replica_count);
 
 /* ---- single stages (for per-operation parity tests and callers that compose stages) ------------- */
 /* J[row, b] for b in [0, floor(t/B)] (eligible blocks); out_scores float32 [Q, num_blocks], entries of
@@ -208,6 +228,59 @@ int hisa_cuda_dense_attend(hisa_cuda_ctx* ctx, const void* query_states, uint32_
                            uint64_t num_queries, double scale, float* out);
 /* device time of the attention kernel of the last sparse/dense attend call (CUDA events on the context's stream) */
 int hisa_cuda_attn_last_ms(hisa_cuda_ctx* ctx, float* ms);
+
+/* ---- multi-GPU: query rows sharded over the GPUs of one box (csrc/dist.cu) -----------------------------
+ * The reference fans rows out over worker threads (hisa/parallel.hpp:15-19; every query row is
+ * independent, the key sequence is shared and read-only). Here the workers are GPUs: keys are replicated by
+ * ncclBroadcast over NVLink, block summaries are recomputed on every GPU, rows are dealt in 512-row tiles zig-zag over
+ * the ranks (causal work grows with the row), and every GPU ends up with the whole [total_rows, token_budget] index
+ * matrix in global row order, bit-identical to a single-GPU run. */
+typedef struct hisa_cuda_dist hisa_cuda_dist;
+#define HISA_DIST_TILE_ROWS 512u
+enum { HISA_DIST_DSA = 0, HISA_DIST_HISA = 1 };
+/* how "every GPU holds every index row" is achieved:
+ *   PEER  the top-k kernel stores each finished row into every GPU's matrix itself (peer stores over NVLink: compute
+ *         and all-gather are one kernel). Needs all ranks in one process and peer access between every pair.
+ *   NCCL  per-tile ncclBroadcast from the tile's owner, in place, grouped per slice on a second stream so that the
+ *         gather of slice i overlaps the kernels of slice i+1.
+ *   AUTO  PEER when possible, else NCCL. */
+enum { HISA_DIST_GATHER_AUTO = 0, HISA_DIST_GATHER_NCCL = 1, HISA_DIST_GATHER_PEER = 2 };
+
+/* Pure index arithmetic, no device needed: the rows rank `rank` of `world` owns among num_rows rows, ascending
+ * (rows_out may be NULL to query only the count). */
+int hisa_cuda_dist_plan(uint64_t num_rows, int world, int rank, uint64_t* count, uint32_t* rows_out);
+/* One process drives num_devices GPUs (ncclCommInitAll, one host thread + context + stream per GPU). flags: gather mode.
+ * A device may be listed several times (logical ranks on one GPU; PEER gather only): used by this library's tests. */
+int hisa_cuda_dist_create(const int* devices, int num_devices, const hisa_cuda_config* cfg, uint32_t flags,
+                          hisa_cuda_dist** out);
+/* One rank of a multi-process job (torchrun / MPI style): rank 0 makes an id (128 bytes) with _unique_id and hands it to
+ * the other ranks by any out-of-band channel; every rank then calls _create_rank (ncclCommInitRank). NCCL gather. */
+int hisa_cuda_dist_unique_id(void* id, size_t bytes);
+int hisa_cuda_dist_create_rank(const void* id, int world, int rank, int device, const hisa_cuda_config* cfg, uint32_t flags,
+                               hisa_cuda_dist** out);
+int hisa_cuda_dist_destroy(hisa_cuda_dist* d);
+/* d == NULL: the calling thread's slot (failures of the create functions and of _plan) */
+const char* hisa_cuda_dist_last_error(const hisa_cuda_dist* d);
+/* world size, ranks living in this process, the first of them, the gather mode in use (any output may be NULL) */
+int hisa_cuda_dist_info(const hisa_cuda_dist* d, int* world, int* num_local, int* first_rank, int* gather);
+/* the single-GPU context of local rank `local` (for pool reads, stage timings, launch counts) */
+hisa_cuda_ctx* hisa_cuda_dist_ctx(hisa_cuda_dist* d, int local);
+/* Replicates the key sequence from rank `root` to every rank and builds the block summaries on each. `keys` (and
+ * key_scales for fp8) are read by the process that owns `root` only: host memory or memory of the root's GPU. */
+int hisa_cuda_dist_upload_keys(hisa_cuda_dist* d, const void* keys, const float* key_scales, uint64_t seq_len, int root);
+/* Sharded selection of total_rows rows. For every LOCAL rank l (index into this process' ranks): queries[l] / gates[l] /
+ * positions[l] hold that rank's rows in hisa_cuda_dist_plan order (device memory of that rank's GPU, or host memory).
+ * num_slices >= 1: a rank's rows run in that many slices of whole tiles (NCCL gather overlaps slice by slice).
+ * Asynchronous: returns when everything is enqueued; results are read with _result after _synchronize (or _fetch). */
+int hisa_cuda_dist_select(hisa_cuda_dist* d, int strategy, const void* const* queries, const float* const* gates,
+                          const uint32_t* const* positions, uint64_t total_rows, int num_slices);
+int hisa_cuda_dist_synchronize(hisa_cuda_dist* d);
+/* device pointers of local rank l's copy of the full result: int32 [total_rows, token_budget] and uint32 [total_rows] */
+int hisa_cuda_dist_result(hisa_cuda_dist* d, int local, int32_t** idx, uint32_t** count);
+/* synchronises and copies local rank l's copy of the result to host memory (either output may be NULL) */
+int hisa_cuda_dist_fetch(hisa_cuda_dist* d, int local, int32_t* host_idx, uint32_t* host_count);
+/* device time of the last _select: first kernel to "this GPU holds every row", maximum over the local ranks */
+int hisa_cuda_dist_last_ms(hisa_cuda_dist* d, float* ms);
 
 /* ---- instrumentation --------------------------------------------------------------------------- */
 typedef struct hisa_cuda_stage_times {

@@ -23,7 +23,14 @@ struct Problem {  // mirrored by oracle/pyoracle.py::Problem
   uint32_t Q, L, H, d;
   uint32_t block_size, block_budget, token_budget;
   uint8_t force_first_last, forced_in_budget, tie_break, pool_mode;
+  uint32_t pool_tokens;  // the BlockSummaryCache covers the first pool_tokens keys (0 = the whole sequence)
 };
+
+// the cache a caller would hold: a snapshot of the first pool_tokens positions (block_summary.hpp:27-30)
+PoolCache cache_of(const Problem& p, const Inputs& in, const Config& cfg) {
+  const uint32_t n = p.pool_tokens ? std::min(p.pool_tokens, in.L) : in.L;
+  return build_block_summaries(in.keys, n, in.d, cfg.block_size, cfg.pool_mode);
+}
 
 Inputs inputs_of(const Problem& p) {
   Inputs in;
@@ -196,7 +203,7 @@ int horacle_score_blocks(const Problem* p, uint32_t row, double* out, uint32_t* 
   return guarded([&] {
     Inputs in = inputs_of(*p);
     Config cfg = config_of(*p);
-    PoolCache cache = build_block_summaries(in.keys, in.L, in.d, cfg.block_size, cfg.pool_mode);
+    PoolCache cache = cache_of(*p, in, cfg);
     OpCounter c;
     ScoreVector sv = score_blocks(in, cache, row, &c);
     std::memcpy(out, sv.scores.data(), sv.scores.size() * sizeof(double));
@@ -252,7 +259,7 @@ int horacle_select_batch(int strategy, const Problem* p, const uint32_t* rows, u
     if (in.L == 0) throw OracleError(Err::EmptySequence, "empty sequence");
     const uint32_t bslots = cfg.block_budget + 2;
     PoolCache cache(cfg.block_size, in.d, cfg.pool_mode);
-    if (strategy != 0) cache = build_block_summaries(in.keys, in.L, in.d, cfg.block_size, cfg.pool_mode);
+    if (strategy != 0) cache = cache_of(*p, in, cfg);
     std::atomic<uint64_t> dots{0};
     parallel_rows(nrows, threads, [&](size_t i) {
       const uint32_t row = rows ? rows[i] : uint32_t(i);
@@ -298,7 +305,7 @@ int horacle_trace_row(int strategy, const Problem* p, uint32_t row, double* J, u
       if (nJ) *nJ = 0;
       if (nblocks) *nblocks = 0;
     } else {
-      PoolCache cache = build_block_summaries(in.keys, in.L, in.d, cfg.block_size, cfg.pool_mode);
+      PoolCache cache = cache_of(*p, in, cfg);
       ScoreVector js = score_blocks(in, cache, row);
       auto sel = select_blocks(js, cfg, t);
       if (J) std::memcpy(J, js.scores.data(), js.scores.size() * sizeof(double));

@@ -45,7 +45,7 @@ class _Problem(C.Structure):
         ("Q", C.c_uint32), ("L", C.c_uint32), ("H", C.c_uint32), ("d", C.c_uint32),
         ("block_size", C.c_uint32), ("block_budget", C.c_uint32), ("token_budget", C.c_uint32),
         ("force_first_last", C.c_uint8), ("forced_in_budget", C.c_uint8), ("tie_break", C.c_uint8),
-        ("pool_mode", C.c_uint8),
+        ("pool_mode", C.c_uint8), ("pool_tokens", C.c_uint32),
     ]
 
 
@@ -132,6 +132,7 @@ class Problem:
     forced_in_budget: bool = False
     tie_break: int = 0   # 0 SmallestIndex, 1 LargestIndex
     pool_mode: int = 0   # 0 Mean, 1 Max
+    pool_tokens: int = 0  # the block-summary cache covers the first pool_tokens keys (0 = all): decode snapshots
 
     def __post_init__(self):
         self.queries = np.ascontiguousarray(self.queries, dtype=np.float32)
@@ -157,6 +158,7 @@ class Problem:
         s.block_size, s.block_budget, s.token_budget = self.block_size, self.block_budget, self.token_budget
         s.force_first_last, s.forced_in_budget = int(self.force_first_last), int(self.forced_in_budget)
         s.tie_break, s.pool_mode = self.tie_break, self.pool_mode
+        s.pool_tokens = self.pool_tokens
         return s
 
 

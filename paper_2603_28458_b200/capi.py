@@ -20,7 +20,11 @@ SCORER_TENSOR, SCORER_SIMT = 0, 1
 
 # every symbol include/hisa_cuda.h declares
 EXPORTED_SYMBOLS = [
-    "hisa_cuda_upload_keys_scaled", "hisa_cuda_pool_append_scaled",
+    "hisa_cuda_upload_keys_scaled", "hisa_cuda_pool_append_scaled", "hisa_cuda_pool_set",
+    "hisa_cuda_set_output_placement", "hisa_cuda_dist_plan", "hisa_cuda_dist_create", "hisa_cuda_dist_unique_id",
+    "hisa_cuda_dist_create_rank", "hisa_cuda_dist_destroy", "hisa_cuda_dist_last_error", "hisa_cuda_dist_info",
+    "hisa_cuda_dist_ctx", "hisa_cuda_dist_upload_keys", "hisa_cuda_dist_select", "hisa_cuda_dist_synchronize",
+    "hisa_cuda_dist_result", "hisa_cuda_dist_fetch", "hisa_cuda_dist_last_ms",
     "hisa_cuda_config_init", "hisa_cuda_config_validate", "hisa_cuda_abi_version", "hisa_cuda_status_name",
     "hisa_cuda_last_error", "hisa_cuda_device_count", "hisa_cuda_create", "hisa_cuda_destroy",
     "hisa_cuda_synchronize", "hisa_cuda_stream", "hisa_cuda_host_alloc", "hisa_cuda_host_free",
@@ -92,6 +96,10 @@ def lib():
         _lib.hisa_cuda_status_name.restype = C.c_char_p
         _lib.hisa_cuda_stream.restype = C.c_void_p
         _lib.hisa_cuda_stream.argtypes = [C.c_void_p]
+        _lib.hisa_cuda_dist_last_error.restype = C.c_char_p
+        _lib.hisa_cuda_dist_last_error.argtypes = [C.c_void_p]
+        _lib.hisa_cuda_dist_ctx.restype = C.c_void_p
+        _lib.hisa_cuda_dist_ctx.argtypes = [C.c_void_p, C.c_int]
     return _lib
 
 
@@ -275,6 +283,13 @@ class Indexer:
 
     def pool_build(self): _check(lib().hisa_cuda_pool_build(self._ctx), self._ctx)
 
+    def pool_set(self, sums, counts, num_tokens):
+        """Installs caller-provided block summaries (BlockSummaryCache contents; may cover fewer tokens than the keys)."""
+        sums = np.ascontiguousarray(sums, dtype=np.float64)
+        counts = np.ascontiguousarray(counts, dtype=np.uint32)
+        _check(lib().hisa_cuda_pool_set(self._ctx, _ptr(sums), _ptr(counts), C.c_uint64(counts.shape[0]),
+                                        C.c_uint64(num_tokens)), self._ctx)
+
     def pool_append(self, keys, n=None, key_dim=None, scales=None):
         keys = self._elems(keys)
         if isinstance(keys, np.ndarray):
@@ -294,8 +309,10 @@ class Indexer:
         _check(lib().hisa_cuda_seq_len(self._ctx, C.byref(L), C.byref(M)), self._ctx)
         return L.value, M.value
 
-    def pool_read(self):
+    def pool_read(self, num_blocks=None):
+        """num_blocks: blocks the current summaries cover when they were installed with pool_set (default: all key blocks)"""
         L, M = self.seq_len()
+        M = M if num_blocks is None else num_blocks
         d = self.cfg.dim
         sums, pooled, counts = np.empty((M, d)), np.empty((M, d)), np.empty(M, np.uint32)
         _check(lib().hisa_cuda_pool_read(self._ctx, _ptr(sums), _ptr(counts), _ptr(pooled)), self._ctx)
@@ -430,6 +447,99 @@ class Indexer:
     def attn_last_ms(self) -> float:
         ms = C.c_float(0.0)
         _check(lib().hisa_cuda_attn_last_ms(self._ctx, C.byref(ms)), self._ctx)
+        return ms.value
+
+
+# ---- multi-GPU driver (hisa_cuda_dist_*) ----------------------------------------------------------------------------
+DIST_DSA, DIST_HISA = 0, 1
+GATHER_AUTO, GATHER_NCCL, GATHER_PEER = 0, 1, 2
+DIST_TILE_ROWS = 512
+
+
+def _dist_check(rc: int, dist=None):
+    if rc != 0:
+        L = lib()
+        msg = L.hisa_cuda_dist_last_error(dist).decode(errors="replace")
+        raise HisaError(rc, L.hisa_cuda_status_name(rc).decode(), msg)
+
+
+def dist_plan(num_rows: int, world: int, rank: int) -> np.ndarray:
+    """Rows rank `rank` of `world` owns (ascending): the C library's own sharding arithmetic, no device needed."""
+    n = C.c_uint64(0)
+    _dist_check(lib().hisa_cuda_dist_plan(C.c_uint64(num_rows), C.c_int(world), C.c_int(rank), C.byref(n), None))
+    rows = np.empty(n.value, np.uint32)
+    _dist_check(lib().hisa_cuda_dist_plan(C.c_uint64(num_rows), C.c_int(world), C.c_int(rank), C.byref(n), _ptr(rows)))
+    return rows
+
+
+def dist_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _dist_check(lib().hisa_cuda_dist_unique_id(buf, C.c_size_t(128)))
+    return bytes(buf)
+
+
+class Dist:
+    """hisa_cuda_dist: query rows sharded over GPUs. Dist(cfg, devices=[...]) drives all GPUs from this process;
+    Dist(cfg, rank=r, world=w, device=d, unique_id=...) is one rank of a multi-process job."""
+
+    def __init__(self, cfg: Config, devices=None, gather=GATHER_AUTO, rank=None, world=None, device=None, unique_id=None):
+        self.cfg = cfg
+        self._d = C.c_void_p(None)
+        if devices is not None:
+            arr = (C.c_int * len(devices))(*devices)
+            _dist_check(lib().hisa_cuda_dist_create(arr, C.c_int(len(devices)), C.byref(cfg), C.c_uint32(gather), C.byref(self._d)))
+        else:
+            idbuf = (C.c_uint8 * 128)(*unique_id)
+            _dist_check(lib().hisa_cuda_dist_create_rank(idbuf, C.c_int(world), C.c_int(rank), C.c_int(device), C.byref(cfg),
+                                                         C.c_uint32(gather), C.byref(self._d)))
+        w, nl, fr, g = C.c_int(0), C.c_int(0), C.c_int(0), C.c_int(0)
+        _dist_check(lib().hisa_cuda_dist_info(self._d, C.byref(w), C.byref(nl), C.byref(fr), C.byref(g)), self._d)
+        self.world, self.num_local, self.first_rank, self.gather = w.value, nl.value, fr.value, g.value
+
+    def close(self):
+        if self._d:
+            lib().hisa_cuda_dist_destroy(self._d)
+            self._d = C.c_void_p(None)
+
+    def __enter__(self): return self
+    def __exit__(self, *a): self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def ctx(self, local: int):
+        return C.c_void_p(lib().hisa_cuda_dist_ctx(self._d, C.c_int(local)))
+
+    def upload_keys(self, keys, seq_len, scales=None, root=0):
+        _dist_check(lib().hisa_cuda_dist_upload_keys(self._d, _ptr(keys), _ptr(scales), C.c_uint64(seq_len), C.c_int(root)), self._d)
+
+    def select(self, strategy, queries, gates, positions, total_rows, num_slices=4):
+        """queries / gates / positions: one entry per LOCAL rank (numpy arrays = host memory, ints = device addresses)"""
+        n = self.num_local
+        qs = (C.c_void_p * n)(*[_ptr(q) for q in queries])
+        ws = (C.c_void_p * n)(*[_ptr(w) for w in gates])
+        ps = (C.c_void_p * n)(*[_ptr(p) for p in positions])
+        _dist_check(lib().hisa_cuda_dist_select(self._d, C.c_int(strategy), qs, ws, ps, C.c_uint64(total_rows), C.c_int(num_slices)), self._d)
+
+    def synchronize(self): _dist_check(lib().hisa_cuda_dist_synchronize(self._d), self._d)
+
+    def result_ptrs(self, local=0):
+        i, c = C.c_void_p(None), C.c_void_p(None)
+        _dist_check(lib().hisa_cuda_dist_result(self._d, C.c_int(local), C.byref(i), C.byref(c)), self._d)
+        return i.value, c.value
+
+    def fetch(self, total_rows, local=0):
+        idx = np.empty((total_rows, self.cfg.token_budget), np.int32)
+        cnt = np.empty(total_rows, np.uint32)
+        _dist_check(lib().hisa_cuda_dist_fetch(self._d, C.c_int(local), _ptr(idx), _ptr(cnt)), self._d)
+        return idx, cnt
+
+    def last_ms(self) -> float:
+        ms = C.c_float(0.0)
+        _dist_check(lib().hisa_cuda_dist_last_ms(self._d, C.byref(ms)), self._d)
         return ms.value
 
 

@@ -10,8 +10,19 @@
 #include <numeric>
 #include <set>
 
-#include "hisa/api.hpp"
+#include "hisa/attention.hpp"
+#include "hisa/audit.hpp"
+#include "hisa/bench.hpp"
+#include "hisa/config.hpp"
+#include "hisa/errors.hpp"
+#include "hisa/hisa.hpp"
+#include "hisa/inputs.hpp"
+#include "hisa/rng.hpp"
+#include "hisa/synth.hpp"
+#include "hisa/types.hpp"
 #include "hisa_cuda.h"
+#include "hisa_gpu.hpp"
+#include "host_util.hpp"
 
 namespace hisa {
 
@@ -34,14 +45,10 @@ hisa_cuda_ctx* C(void* p) { return static_cast<hisa_cuda_ctx*>(p); }
 void check(void* ctx, int status) {
   if (status != HISA_OK) raise_status(status, hisa_cuda_last_error(C(ctx)));
 }
-std::vector<uint16_t> to_bf16(const std::vector<float>& v) {
-  std::vector<uint16_t> out(v.size());
-  for (size_t i = 0; i < v.size(); ++i) {
-    uint32_t u;
-    std::memcpy(&u, &v[i], 4);
-    out[i] = uint16_t((u + ((u >> 16) & 1u) + 0x7FFFu) >> 16);
-  }
-  return out;
+using detail::to_bf16;
+// the whole latent table / all query states as one span (the reference exposes rows only, attention.hpp:31-36)
+std::span<const float> all_latents(const AttentionInputs& a) {
+  return a.seq_len() ? std::span<const float>(a.latent(0).data(), size_t(a.seq_len()) * a.d_model()) : std::span<const float>();
 }
 
 }  // namespace
@@ -87,11 +94,16 @@ Attention::Attention(const AttentionInputs& attn, Storage storage, int device) :
   ctx_ = ctx;
   if (attn.seq_len() == 0) return;  // attending then reports EmptySequence
   int st;
+  if (storage == Storage::FP8) {
+    hisa_cuda_destroy(ctx);
+    ctx_ = nullptr;
+    throw Error("attention: latent states are stored as float32 or bfloat16");
+  }
   if (storage == Storage::BF16) {
-    const auto b = to_bf16(attn.latent_states_raw());
+    const auto b = to_bf16(all_latents(attn));
     st = hisa_cuda_attn_set_latents(ctx, b.data(), attn.seq_len(), attn.d_model(), HISA_DTYPE_BF16, 0);
   } else {
-    st = hisa_cuda_attn_set_latents(ctx, attn.latent_states_raw().data(), attn.seq_len(), attn.d_model(), HISA_DTYPE_F32, 0);
+    st = hisa_cuda_attn_set_latents(ctx, all_latents(attn).data(), attn.seq_len(), attn.d_model(), HISA_DTYPE_F32, 0);
   }
   if (st != HISA_OK) {
     const std::string msg = hisa_cuda_last_error(ctx);
@@ -197,20 +209,23 @@ float Attention::last_kernel_ms() {
 // ==================================================================================================
 namespace {
 std::mutex g_attn_mu;
-const AttentionInputs* g_attn_key = nullptr;
-const float* g_attn_data = nullptr;
-size_t g_attn_size = 0;
+uint64_t g_attn_hash = 0;
+uint32_t g_attn_len = 0, g_attn_dm = 0;
 std::unique_ptr<gpu::Attention> g_attn_ctx;
 
+// The latent table is uploaded once per latent CONTENT: the key is a hash of the whole table, never the object's
+// address (a new AttentionInputs built where a destroyed one lived must not be served the old table). O(table) per
+// call; bulk callers use gpu::Attention.
 gpu::Attention& attention_for(const AttentionInputs& a) {
-  // the latent table is uploaded once per AttentionInputs object (immutable after construction)
-  if (g_attn_key != &a || g_attn_data != a.latent_states_raw().data() || g_attn_size != a.latent_states_raw().size()) {
+  const uint64_t h = detail::hash_span(all_latents(a), 3);
+  if (!g_attn_ctx || g_attn_hash != h || g_attn_len != a.seq_len() || g_attn_dm != a.d_model()) {
     g_attn_ctx.reset();
     g_attn_ctx = std::make_unique<gpu::Attention>(a, gpu::Storage::F32);
-    g_attn_key = &a;
-    g_attn_data = a.latent_states_raw().data();
-    g_attn_size = a.latent_states_raw().size();
+    g_attn_hash = h;
+    g_attn_len = a.seq_len();
+    g_attn_dm = a.d_model();
   }
+  g_attn_ctx->rebind(a);  // rows and positions are read from the caller's object of THIS call
   return *g_attn_ctx;
 }
 }  // namespace
@@ -276,8 +291,7 @@ std::string list_head(const std::vector<uint32_t>& v) {
 }
 
 void fail_report(AuditReport& rep, uint64_t seed, uint32_t row, std::string detail) {
-  if (rep.failed) return;
-  rep.failed = true;
+  if (rep.failure) return;
   rep.failure = AuditFailure{seed, row, std::move(detail)};
 }
 
@@ -287,7 +301,7 @@ constexpr uint32_t kAuditQueries = 64;
 
 AuditReport run_regime_equivalence_audit(const AuditOptions& opt) {
   AuditReport rep;
-  for (uint32_t i = 0; rep.queries_checked < opt.min_queries && !rep.failed; ++i) {
+  for (uint32_t i = 0; rep.queries_checked < opt.min_queries && rep.passed(); ++i) {
     const uint64_t seed = mix_seed(opt.base_seed, i, 0x5245u);
     Instance inst = draw_instance(seed, Regime::FlatEquivalent, kAuditQueries);
     Rng rng(mix_seed(seed, 1));
@@ -310,7 +324,7 @@ AuditReport run_regime_equivalence_audit(const AuditOptions& opt) {
     const auto a = hier.hisa_select_batch(in);
     const auto b = flat.dsa_select_batch(in);
     ++rep.instances_run;
-    for (uint32_t r = 0; r < in.num_queries() && !rep.failed; ++r) {
+    for (uint32_t r = 0; r < in.num_queries() && rep.passed(); ++r) {
       ++rep.queries_checked;
       if (a[r].token_indices != b[r].token_indices)
         fail_report(rep, seed, r, "t=" + std::to_string(in.position(r)) + " <= mB-1 but hisa " + list_head(a[r].token_indices) +
@@ -322,7 +336,7 @@ AuditReport run_regime_equivalence_audit(const AuditOptions& opt) {
 
 AuditReport run_dense_regime_audit(const AuditOptions& opt) {
   AuditReport rep;
-  for (uint32_t i = 0; rep.queries_checked < opt.min_queries && !rep.failed; ++i) {
+  for (uint32_t i = 0; rep.queries_checked < opt.min_queries && rep.passed(); ++i) {
     const uint64_t seed = mix_seed(opt.base_seed, i, 0x4445u);
     const Instance inst = draw_instance(seed, Regime::Dense, kAuditQueries);
     Rng rng(mix_seed(seed, 1));
@@ -331,7 +345,7 @@ AuditReport run_dense_regime_audit(const AuditOptions& opt) {
     ix.set_keys(in.keys_raw());
     const std::vector<SelectionResult> res[3] = {ix.dsa_select_batch(in), ix.hisa_select_batch(in), ix.block_sparse_select_batch(in)};
     ++rep.instances_run;
-    for (uint32_t r = 0; r < in.num_queries() && !rep.failed; ++r) {
+    for (uint32_t r = 0; r < in.num_queries() && rep.passed(); ++r) {
       ++rep.queries_checked;
       std::vector<uint32_t> prefix(in.position(r) + 1);
       std::iota(prefix.begin(), prefix.end(), 0u);
@@ -346,7 +360,7 @@ AuditReport run_dense_regime_audit(const AuditOptions& opt) {
 
 AuditReport run_subset_chain_audit(const AuditOptions& opt) {
   AuditReport rep;
-  for (uint32_t i = 0; rep.queries_checked < opt.min_queries && !rep.failed; ++i) {
+  for (uint32_t i = 0; rep.queries_checked < opt.min_queries && rep.passed(); ++i) {
     const uint64_t seed = mix_seed(opt.base_seed, i, 0x5343u);
     const Instance inst = draw_instance(seed, Regime::Unrestricted, kAuditQueries);
     Rng rng(mix_seed(seed, 1));
@@ -359,7 +373,7 @@ AuditReport run_subset_chain_audit(const AuditOptions& opt) {
     const auto again = ix.hisa_select_batch(in);
     ++rep.instances_run;
     uint64_t bound = 0;
-    for (uint32_t r = 0; r < in.num_queries() && !rep.failed; ++r) {
+    for (uint32_t r = 0; r < in.num_queries() && rep.passed(); ++r) {
       ++rep.queries_checked;
       const SelectionResult& s = first[r];
       const uint32_t t = in.position(r), B = cfg.block_size;
@@ -380,7 +394,7 @@ AuditReport run_subset_chain_audit(const AuditOptions& opt) {
         bad("forced first/last block missing");
       if (again[r].token_indices != s.token_indices || again[r].selected_blocks != s.selected_blocks) bad("second run differs (determinism)");
     }
-    if (!rep.failed && ops.dot_products > bound)
+    if (rep.passed() && ops.dot_products > bound)
       fail_report(rep, seed, 0, "dot products " + std::to_string(ops.dot_products) + " exceed the analytic bound " + std::to_string(bound));
   }
   return rep;

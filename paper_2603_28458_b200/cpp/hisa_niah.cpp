@@ -8,7 +8,14 @@
 #include <memory>
 #include <ostream>
 
-#include "hisa/api.hpp"
+#include "hisa/config.hpp"
+#include "hisa/errors.hpp"
+#include "hisa/inputs.hpp"
+#include "hisa/niah.hpp"
+#include "hisa/rng.hpp"
+#include "hisa/synth.hpp"
+#include "hisa/types.hpp"
+#include "hisa_gpu.hpp"
 
 namespace hisa {
 

@@ -14,8 +14,10 @@
 #include "hisa/bench.hpp"
 #include "hisa/hisa.hpp"
 #include "hisa/niah.hpp"
+#include "hisa/parallel.hpp"
 #include "hisa/synth.hpp"
 #include "hisa/tensor_io.hpp"
+#include "hisa_gpu.hpp"
 
 using namespace hisa;
 
@@ -186,6 +188,143 @@ int main() {
       EXPECT(bs.token_indices == omega);
     }
   }
+  // ---- the caller's BlockSummaryCache is what gets scored (hisa.hpp:16-21, block_summary.hpp:27-30) ----
+  {
+    Rng rng(31);
+    const uint32_t L = 1000, H = 2, d = 8, B = 64, m = 3, k = 100;
+    auto in = make_random_inputs(rng, L, std::vector<uint32_t>{10, 250, 299, 300, 640, 999}, H, d);
+    HisaConfig cfg(B, m, k, H, d);
+    // (a) a snapshot shorter than the inputs: 300 tokens appended = 5 blocks (the last one partial)
+    BlockSummaryCache part(B, d);
+    for (uint32_t s = 0; s < 300; ++s) part.append(in.key(s));
+    EXPECT(part.num_blocks() == 5 && part.num_tokens() == 300);
+    for (uint32_t r = 0; r < in.num_queries(); ++r) {
+      const uint32_t t = in.position(r), elig = std::min(t / B, 4u) + 1;
+      auto J = score_blocks(in, part, r);
+      EXPECT(J.scores.size() == elig);  // eligible blocks clipped to cache.num_blocks()
+      double worst = 0;
+      for (uint32_t b = 0; b < elig; ++b) {
+        const auto pk = part.pooled(b);
+        double acc = 0;
+        for (uint32_t j = 0; j < H; ++j) {
+          double dp = 0;
+          for (uint32_t i = 0; i < d; ++i) dp += double(in.query(r, j)[i]) * pk[i];
+          acc += double(in.gate(r, j)) * std::max(dp, 0.0);
+        }
+        worst = std::max(worst, std::abs(acc - J.scores[b]));
+      }
+      EXPECT(worst < 1e-5);
+      auto h = hisa_select(in, part, cfg, r);
+      EXPECT(!h.selected_blocks.empty() && h.selected_blocks.front() == 0 && h.selected_blocks.back() == elig - 1);
+      auto omega = candidate_union(h.selected_blocks, B, t, L);
+      EXPECT(h.candidate_size == omega.size() && h.token_indices.size() == std::min<size_t>(k, omega.size()));
+      EXPECT(std::includes(omega.begin(), omega.end(), h.token_indices.begin(), h.token_indices.end()));
+      EXPECT(block_sparse_select(in, part, cfg, r).token_indices == omega);
+    }
+    // (b) a cache that was fed DIFFERENT keys: its contents decide the block scores, not the inputs' keys
+    BlockSummaryCache other(B, d);
+    for (uint32_t s = 0; s < L; ++s) {
+      std::vector<float> kk(in.key(s).begin(), in.key(s).end());
+      if (s / B == 2) for (auto& v : kk) v = -v;
+      other.append(kk);
+    }
+    auto full = build_block_summaries(in.keys_raw(), d, B);
+    auto Ja = score_blocks(in, full, 5), Jb = score_blocks(in, other, 5);
+    EXPECT(Ja.scores.size() == 16 && Jb.scores.size() == 16);
+    EXPECT(Ja.scores[2] != Jb.scores[2] && Ja.scores[1] == Jb.scores[1] && Ja.scores[3] == Jb.scores[3]);
+    EXPECT(throws<EmptySequence>([&] { BlockSummaryCache empty(B, d); score_blocks(in, empty, 0); }));
+  }
+  // ---- per-row calls fanned out over threads (parallel.hpp:15-19; SPEC "callers may fan out queries") ----
+  {
+    Rng rng(41);
+    const uint32_t L = 2048, H = 4, d = 16, B = 32, m = 4, k = 64, Q = 96;
+    auto in = make_random_inputs(rng, L, Q, H, d, QueryPlacement::Spread);
+    HisaConfig cfg(B, m, k, H, d);
+    auto cache = build_block_summaries(in.keys_raw(), d, B);
+    std::vector<SelectionResult> par(Q), par_flat(Q);
+    parallel_for(Q, 8, [&](std::size_t r) {
+      par[r] = hisa_select(in, cache, cfg, uint32_t(r));
+      par_flat[r] = dsa_select(in, cfg, uint32_t(r));
+    });
+    bool same = true;
+    for (uint32_t r = 0; r < Q; ++r) {
+      same = same && par[r].token_indices == hisa_select(in, cache, cfg, r).token_indices;
+      same = same && par_flat[r].token_indices == dsa_select(in, cfg, r).token_indices;
+    }
+    EXPECT(same);
+  }
+  // ---- results follow the CONTENT of the inputs, not their address (same sizes, one key row differs) ----
+  {
+    const uint32_t L = 512, H = 2, d = 8;
+    HisaConfig cfg(32, 2, 16, H, d);
+    std::vector<std::vector<uint32_t>> got;
+    for (int variant = 0; variant < 2; ++variant) {
+      Rng rng(51);  // same seed: identical tensors ...
+      IndexerInputs base = make_random_inputs(rng, L, std::vector<uint32_t>{L - 1}, H, d);
+      std::vector<float> keys = base.keys_raw();
+      const uint32_t needle = variant ? 300u : 100u;  // ... except for one boosted key row
+      for (uint32_t i = 0; i < d; ++i) keys[needle * d + i] = 40.f * base.query(0, 0)[i];
+      const IndexerInputs in(base.queries_raw(), base.gates_raw(), std::move(keys), base.positions_raw(), H, d);
+      got.push_back(dsa_select(in, cfg, 0).token_indices);
+      EXPECT(std::binary_search(got.back().begin(), got.back().end(), needle));
+    }
+    EXPECT(got[0] != got[1]);
+  }
+  // ---- double scores that collapse to one float are still ordered by their double value (dsa.hpp:22-27) ----
+  {
+    ScoreVector sv{{1.0, 1.0 + 1e-12, 1.0 + 2e-12, 0.5}, {0, 1, 2, 3}};
+    EXPECT((top_k_tokens(sv, 1, TieBreak::SmallestIndex).token_indices == std::vector<uint32_t>{2}));
+    EXPECT((top_k_tokens(sv, 2, TieBreak::SmallestIndex).token_indices == std::vector<uint32_t>{1, 2}));
+    Rng rng(61);
+    for (int trial = 0; trial < 10; ++trial) {
+      ScoreVector v;
+      const uint32_t n = 200 + uint32_t(rng.below(800));
+      for (uint32_t i = 0; i < n; ++i) { v.scores.push_back(1.0 + 1e-9 * double(rng.below(50))); v.positions.push_back(i); }
+      const TieBreak tb = trial % 2 ? TieBreak::SmallestIndex : TieBreak::LargestIndex;
+      EXPECT(top_k_tokens(v, 37, tb).token_indices == naive_topk(v.scores, v.positions, 37, tb));
+      HisaConfig cfg(4, 9, 8, 1, 2);
+      cfg.tie_break = tb;
+      cfg.forced_in_budget = trial % 3 == 0;
+      auto blocks = select_blocks(v, cfg, (n - 1) * 4);
+      std::vector<double> rest(v.scores);
+      std::vector<uint32_t> want;
+      if (cfg.forced_in_budget) {
+        std::vector<double> mid(v.scores.begin() + 1, v.scores.end() - 1);
+        std::vector<uint32_t> mp(v.positions.begin() + 1, v.positions.end() - 1);
+        want = naive_topk(mid, mp, 7, tb);
+      } else {
+        want = naive_topk(v.scores, v.positions, 9, tb);
+      }
+      want.push_back(0);
+      want.push_back(n - 1);
+      std::sort(want.begin(), want.end());
+      want.erase(std::unique(want.begin(), want.end()), want.end());
+      EXPECT(blocks == want);
+    }
+  }
+  // ---- fp8 storage through the C++ layer, the 4:1 sweep and the separately reported pool build ----
+  {
+    Rng rng(71);
+    const uint32_t L = 2048, H = 64, d = 128, B = 64, m = 4, k = 128;
+    auto in = make_random_inputs(rng, L, std::vector<uint32_t>{100, 700, 1500, 2047}, H, d);
+    HisaConfig cfg(B, m, k, H, d);
+    gpu::Indexer f8(cfg, gpu::Storage::FP8), bf(cfg, gpu::Storage::BF16);
+    f8.set_keys(in.keys_raw());
+    bf.set_keys(in.keys_raw());
+    auto a = f8.hisa_select_batch(in), b = bf.hisa_select_batch(in);
+    double iou = 0;
+    for (uint32_t r = 0; r < in.num_queries(); ++r) {
+      EXPECT(a[r].token_indices.size() == b[r].token_indices.size() && std::is_sorted(a[r].token_indices.begin(), a[r].token_indices.end()));
+      iou += selection_overlap(a[r], b[r]);
+    }
+    EXPECT(iou / in.num_queries() > 0.6);  // e4m3 quantisation moves the boundary, not the bulk of the selection
+    HisaConfig small(32, 4, 64, 4, 16);
+    const uint32_t lengths[] = {1024, 4096};
+    const Strategy strategies[] = {Strategy::Dsa, Strategy::Hisa};
+    auto sweep = gpu::run_bench_sweep(small, lengths, 8, 1, strategies, gpu::SweepMode::Ratio, 4);
+    EXPECT(sweep.size() == 4 && sweep[0].block_budget == 8 && sweep[2].block_budget == 32 && sweep[3].strategy == Strategy::Hisa);
+    EXPECT(sweep[1].pool_build_ns > 0 && sweep[3].wall_ns_median > 0);  // bench.hpp:28
+  }
   // ---- analytic cost and the bench record ----
   {
     HisaConfig cfg(128, 64, 2048, 1, 16);
@@ -289,17 +428,18 @@ int main() {
     AuditOptions ao;
     ao.min_queries = 300;
     auto a = run_regime_equivalence_audit(ao);
-    if (!a.passed()) std::printf("regime audit: seed %llu row %u %s\n", (unsigned long long)a.failure.instance_seed, a.failure.query_row, a.failure.detail.c_str());
+    if (!a.passed()) std::printf("regime audit: seed %llu row %u %s\n", (unsigned long long)a.failure->instance_seed, a.failure->query_row, a.failure->detail.c_str());
     EXPECT(a.passed() && a.queries_checked >= 300 && a.instances_run >= 1);
     auto b = run_dense_regime_audit(ao);
-    if (!b.passed()) std::printf("dense audit: seed %llu row %u %s\n", (unsigned long long)b.failure.instance_seed, b.failure.query_row, b.failure.detail.c_str());
+    if (!b.passed()) std::printf("dense audit: seed %llu row %u %s\n", (unsigned long long)b.failure->instance_seed, b.failure->query_row, b.failure->detail.c_str());
     EXPECT(b.passed() && b.queries_checked >= 300);
     auto c = run_subset_chain_audit(ao);
-    if (!c.passed()) std::printf("subset audit: seed %llu row %u %s\n", (unsigned long long)c.failure.instance_seed, c.failure.query_row, c.failure.detail.c_str());
+    if (!c.passed()) std::printf("subset audit: seed %llu row %u %s\n", (unsigned long long)c.failure->instance_seed, c.failure->query_row, c.failure->detail.c_str());
     EXPECT(c.passed() && c.queries_checked >= 300);
     ao.inject_tie_mismatch = true;  // the failure path must fire
     auto f = run_regime_equivalence_audit(ao);
-    EXPECT(!f.passed() && !f.failure.detail.empty());
+    EXPECT(!f.passed() && f.failure.has_value() && !f.failure->detail.empty());  // audit.hpp:23-24
+    EXPECT(!a.failure.has_value());
     AblationOptions ab;
     ab.seq_len = 4096;
     ab.token_budget = 512;

@@ -12,7 +12,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/hisa_cuda.h"
@@ -56,11 +59,22 @@ struct hisa_cuda_ctx {
   // sequence state
   uint64_t seq_len = 0, key_cap = 0;
   uint64_t pooled_tokens = 0;  // tokens folded into the summaries so far
+  // summaries installed by hisa_cuda_pool_set (a BlockSummaryCache snapshot that may cover fewer tokens than the key
+  // sequence, hisa/hisa.hpp:16-21): eligibility is clipped to pool_blocks and the keys are not re-pooled
+  bool pool_external = false;
+  uint64_t pool_blocks = 0;
   DevBuf key_op, key_raw, key_scale, sums, counts, pooled_op;
 
   // per-call workspace
   DevBuf q_raw, q_op, gates_raw, gates_pad, pos, J, sel, nsel, work, pairs, scalars, cand, flat, out_idx, out_count,
-      out_cand, generic_scores, generic_n, export_a, export_b, flag, stats;
+      out_cand, generic_scores, generic_n, export_a, export_b, flag, stats, inv_scratch;
+
+  // output placement for row-sharded multi-GPU runs (hisa_cuda_set_output_placement)
+  const uint32_t* place_rows = nullptr;
+  uint64_t place_q0 = 0;  // first row of the current host-pipeline slice inside the call (select_pipelined)
+  uint32_t place_nrep = 0;
+  int32_t* place_rep_idx[kMaxReplicas] = {};
+  uint32_t* place_rep_count[kMaxReplicas] = {};
 
   // downstream consumer (attention.hpp): latent table + per-call staging
   DevBuf attn_lat, attn_q, attn_qraw, attn_pos, attn_idx, attn_cnt, attn_out, attn_w;
@@ -224,6 +238,10 @@ int make_map(hisa_cuda_ctx* ctx, CUtensorMap* map, const void* base, uint64_t ro
 
 uint64_t num_blocks_of(const hisa_cuda_ctx* ctx) {
   return (ctx->seq_len + ctx->cfg.block_size - 1) / ctx->cfg.block_size;
+}
+// blocks the current summaries cover: eligible blocks of a query are [0, floor(t/B)] clipped to this (hisa.hpp:16-21)
+uint64_t pool_blocks_of(const hisa_cuda_ctx* ctx) {
+  return ctx->pool_external ? std::min<uint64_t>(ctx->pool_blocks, num_blocks_of(ctx)) : num_blocks_of(ctx);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -410,7 +428,7 @@ void set_token_operands(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, Scor
 }
 
 int ensure_pool(hisa_cuda_ctx* ctx) {
-  if (ctx->pooled_tokens == ctx->seq_len) return HISA_OK;
+  if (ctx->pool_external || ctx->pooled_tokens == ctx->seq_len) return HISA_OK;
   return hisa_cuda_pool_build(ctx);
 }
 
@@ -438,7 +456,7 @@ uint32_t list_chunk_for(const hisa_cuda_ctx* ctx, uint64_t nq) {
 
 // stage 1: J[q, b] for rows [0, nq) -> ctx->J with stride Mpad
 int run_score_blocks(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, uint64_t nq, uint32_t Mpad) {
-  const uint32_t M = uint32_t(num_blocks_of(ctx));
+  const uint32_t M = uint32_t(pool_blocks_of(ctx));
   const uint32_t ntiles = Mpad / kTileRows;
   const uint32_t chunk = dense_chunk_for(ctx, nq, ntiles);
   const uint32_t nchunks = uint32_t((nq + chunk - 1) / chunk);
@@ -473,7 +491,7 @@ int run_select_blocks(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, uint64
   s.stride = Mpad;
   s.pos = p.pos + q0;
   s.seq_len = uint32_t(ctx->seq_len);
-  s.num_blocks = uint32_t(num_blocks_of(ctx));
+  s.num_blocks = uint32_t(pool_blocks_of(ctx));
   s.block_size = ctx->cfg.block_size;
   s.keep = ctx->cfg.block_budget;
   s.mode = kSelBlocks;
@@ -530,7 +548,7 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
   const hisa_cuda_config& c = ctx->cfg;
   const uint32_t B = c.block_size, S = c.block_budget + 2, k = c.token_budget;
   const uint32_t L = uint32_t(ctx->seq_len);
-  const uint32_t M = uint32_t(num_blocks_of(ctx));
+  const uint32_t M = uint32_t(strat == kDsa ? num_blocks_of(ctx) : pool_blocks_of(ctx));
   const uint32_t Mpad = round_up(M, kTileRows);
   const uint32_t Lpad = round_up(L, kTileRows);
   const uint32_t out_width = strat == kBlockSparse ? S * B : k;
@@ -560,11 +578,28 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
     if (!nblk_dev) HISA_TRY(ensure(ctx, ctx->nsel, size_t(pass_rows) * 4));
   }
 
+  // placed output: row i of the call lands at row place_rows[i] of the caller's (full-size) device arrays
+  const bool placed = (ctx->place_rows || ctx->place_nrep) && strat != kBlockSparse;
+  if (placed && (!idx_dev || (out_count && !cnt_dev) || (out_cand && !cand_dev)))
+    return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "output placement needs device output arrays");
+  auto place = [&](SelectArgs& s, uint64_t q0) {
+    if (!placed) return;
+    const uint64_t first = ctx->place_q0 + q0;  // row of the API call this launch starts at
+    s.out_rows = ctx->place_rows ? ctx->place_rows + first : nullptr;
+    s.n_rep = ctx->place_nrep;
+    for (uint32_t r = 0; r < ctx->place_nrep; ++r) {
+      // without a row map the replicas are indexed like the local arrays: by the row of the call
+      s.rep_out[r] = ctx->place_rep_idx[r] + (ctx->place_rows ? 0 : first * out_width);
+      s.rep_count[r] = ctx->place_rep_count[r] ? ctx->place_rep_count[r] + (ctx->place_rows ? 0 : first) : nullptr;
+    }
+  };
+
   for (uint64_t q0 = 0; q0 < Q; q0 += pass_rows) {
     const uint64_t nq = std::min<uint64_t>(pass_rows, Q - q0);
-    int32_t* idx_dst = idx_dev ? out_idx + q0 * out_width : ctx->out_idx.as<int32_t>();
-    uint32_t* cnt_dst = cnt_dev ? out_count + q0 : ctx->out_count.as<uint32_t>();
-    uint32_t* cand_dst = cand_dev ? out_cand + q0 : ctx->out_cand.as<uint32_t>();
+    const bool mapped = placed && ctx->place_rows;  // the row map already addresses the full arrays
+    int32_t* idx_dst = idx_dev ? out_idx + (mapped ? 0 : q0 * out_width) : ctx->out_idx.as<int32_t>();
+    uint32_t* cnt_dst = cnt_dev ? out_count + (mapped ? 0 : q0) : (placed ? nullptr : ctx->out_count.as<uint32_t>());
+    uint32_t* cand_dst = cand_dev ? out_cand + (mapped ? 0 : q0) : (placed ? nullptr : ctx->out_cand.as<uint32_t>());
 
     if (strat == kDsa) {
       // ---- flat indexer: score the whole causal prefix, then top-k (dsa.hpp:29-32) ----
@@ -607,6 +642,7 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
         s.out_width = out_width;
         s.out_count = cnt_dst;
         s.out_cand = cand_dst;
+        place(s, q0);
         count_launches(ctx, launch_select(s, uint32_t(nq), L, ctx->stream));
         HISA_TRY(check_launch(ctx, "top-k"));
       }
@@ -639,12 +675,17 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
         HISA_TRY(ensure(ctx, ctx->work, size_t(items_cap) * sizeof(WorkItem)));
         HISA_TRY(ensure(ctx, ctx->pairs, size_t(nchunks) * chunk_list * S * sizeof(uint2)));
         HISA_TRY(ensure(ctx, ctx->cand, size_t(nq) * cand_cols * 4));
+        const size_t inv_words = invert_global_words(uint32_t(nq), chunk_list, M);
+        if (inv_words) HISA_TRY(ensure(ctx, ctx->inv_scratch, inv_words * sizeof(uint32_t)));
         uint32_t* sc = ctx->scalars.as<uint32_t>();
         {
           StageTimer timer(ctx, kStInvert);
-          count_launches(ctx, launch_invert_selection(sel, nsel, S, uint32_t(nq), chunk_list, M, B, spb, split,
-                                                      ctx->work.as<WorkItem>(), sc, sc + 1, ctx->pairs.as<uint2>(),
-                                                      ctx->stream));
+          const int n_inv = launch_invert_selection(sel, nsel, S, uint32_t(nq), chunk_list, M, B, spb, split,
+                                                    ctx->work.as<WorkItem>(), sc, sc + 1, ctx->pairs.as<uint2>(),
+                                                    inv_words ? ctx->inv_scratch.as<uint32_t>() : nullptr, ctx->stream);
+          if (n_inv < 0)
+            return fail(ctx, HISA_ERR_UNSUPPORTED, "invert selection: %u key blocks need more shared memory than an SM has", M);
+          count_launches(ctx, n_inv);
           HISA_TRY(check_launch(ctx, "invert selection"));
         }
         {
@@ -682,6 +723,7 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
           s.out_width = out_width;
           s.out_count = cnt_dst;
           s.out_cand = cand_dst;
+          place(s, q0);
           count_launches(ctx, launch_select(s, uint32_t(nq), uint32_t(std::min<uint64_t>(cand_cols, L)), ctx->stream));
           HISA_TRY(check_launch(ctx, "top-k"));
         }
@@ -779,9 +821,12 @@ int select_pipelined(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, co
     const void* q_s = q_host ? ctx->st_q[b].p : static_cast<const void*>(static_cast<const char*>(queries) + q0 * q_row);
     const float* g_s = g_host ? ctx->st_g[b].as<float>() : gates + q0 * H;
     const uint32_t* p_s = p_host ? ctx->st_pos[b].as<uint32_t>() : positions + q0;
-    int32_t* idx_s = idx_host ? ctx->st_idx[b].as<int32_t>() : out_idx + q0 * out_width;
-    uint32_t* cnt_s = !out_count ? nullptr : cnt_host ? ctx->st_cnt[b].as<uint32_t>() : out_count + q0;
-    uint32_t* cand_s = !out_cand ? nullptr : cand_host ? ctx->st_cand[b].as<uint32_t>() : out_cand + q0;
+    // a row map addresses the caller's full device arrays: no per-slice offset on them, the map is offset instead
+    const bool mapped = ctx->place_rows != nullptr && strat != kBlockSparse;
+    int32_t* idx_s = idx_host ? ctx->st_idx[b].as<int32_t>() : out_idx + (mapped ? 0 : q0 * out_width);
+    uint32_t* cnt_s = !out_count ? nullptr : cnt_host ? ctx->st_cnt[b].as<uint32_t>() : out_count + (mapped ? 0 : q0);
+    uint32_t* cand_s = !out_cand ? nullptr : cand_host ? ctx->st_cand[b].as<uint32_t>() : out_cand + (mapped ? 0 : q0);
+    ctx->place_q0 = q0;
     int32_t* blk_s = (strat == kDsa || !out_blocks) ? nullptr : blk_host ? ctx->st_blk[b].as<int32_t>() : out_blocks + q0 * S;
     uint32_t* nblk_s = (strat == kDsa || !out_nblocks) ? nullptr : nblk_host ? ctx->st_nblk[b].as<uint32_t>() : out_nblocks + q0;
     mark(ctx->stream);
@@ -800,6 +845,7 @@ int select_pipelined(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, co
     CU_TRY(ctx, cudaEventRecord(ctx->ev_out_free[b], ctx->out_stream));
     mark(ctx->out_stream);
   }
+  ctx->place_q0 = 0;
   CU_TRY(ctx, cudaStreamSynchronize(ctx->out_stream));
   CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   if (trace) {
@@ -830,6 +876,7 @@ int select_impl(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
   if (!out_idx && Q) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "out_idx must be non-null");
   CU_TRY(ctx, cudaSetDevice(ctx->device));
   begin_call(ctx);
+  ctx->place_q0 = 0;
   if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "selection over an empty key sequence");
   if (strat != kDsa) HISA_TRY(ensure_pool(ctx));
   if (Q && (!queries || !gates || !positions))
@@ -857,6 +904,27 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 }
 
 }  // namespace
+
+namespace hisa_dev {
+bool smem_opt_in(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;  // (device, kernel) -> bytes already granted
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  std::lock_guard<std::mutex> g(mu);
+  size_t& have = done[{dev, func}];
+  if (have >= bytes) return true;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  have = bytes;
+  return true;
+}
+}  // namespace hisa_dev
 
 // ==================================================================================================
 // C ABI
@@ -1006,6 +1074,7 @@ int hisa_cuda_destroy(hisa_cuda_ctx* ctx) {
                     &ctx->gates_raw, &ctx->gates_pad, &ctx->pos, &ctx->J, &ctx->sel, &ctx->nsel, &ctx->work, &ctx->pairs,
                     &ctx->scalars, &ctx->cand, &ctx->flat, &ctx->out_idx, &ctx->out_count, &ctx->out_cand,
                     &ctx->generic_scores, &ctx->generic_n, &ctx->export_a, &ctx->export_b, &ctx->flag, &ctx->stats,
+                    &ctx->inv_scratch,
                     &ctx->attn_lat, &ctx->attn_q, &ctx->attn_qraw, &ctx->attn_pos, &ctx->attn_idx, &ctx->attn_cnt,
                     &ctx->attn_out, &ctx->attn_w})
     release(*b);
@@ -1163,6 +1232,7 @@ static int upload_keys_impl(hisa_cuda_ctx* ctx, const void* keys, const float* s
   if (seq_len > 0x7FFFFF00ull) return fail(ctx, HISA_ERR_UNSUPPORTED, "sequence too long");
   ctx->seq_len = 0;
   ctx->pooled_tokens = 0;
+  ctx->pool_external = false;
   HISA_TRY(grow_keys(ctx, seq_len));
   HISA_TRY(ingest_keys(ctx, keys, scales, 0, seq_len, check_finite));
   ctx->seq_len = seq_len;
@@ -1177,7 +1247,8 @@ static int pool_append_impl(hisa_cuda_ctx* ctx, const void* keys, const float* s
   if (n == 0) return HISA_OK;
   if (!keys) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "null keys");
   if (scales && !ctx->fp8) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "key scales are only meaningful for fp8 storage");
-  if (ctx->pooled_tokens != ctx->seq_len) HISA_TRY(hisa_cuda_pool_build(ctx));
+  // installed snapshots (hisa_cuda_pool_set) are replaced by summaries of the keys the context holds
+  if (ctx->pool_external || ctx->pooled_tokens != ctx->seq_len) HISA_TRY(hisa_cuda_pool_build(ctx));
   HISA_TRY(grow_keys(ctx, ctx->seq_len + n));
   HISA_TRY(ingest_keys(ctx, keys, scales, ctx->seq_len, n, 0));
   HISA_TRY(pool_update(ctx, ctx->seq_len, n));
@@ -1201,7 +1272,45 @@ int hisa_cuda_pool_build(hisa_cuda_ctx* ctx) {
   if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "build_block_summaries: key matrix has no rows");
   HISA_TRY(pool_update(ctx, 0, ctx->seq_len));
   ctx->pooled_tokens = ctx->seq_len;
+  ctx->pool_external = false;
   return check_launch(ctx, "pool build");
+}
+
+int hisa_cuda_pool_set(hisa_cuda_ctx* ctx, const double* sums, const uint32_t* counts, uint64_t num_blocks,
+                       uint64_t num_tokens) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  CU_TRY(ctx, cudaSetDevice(ctx->device));
+  if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "pool_set: upload the key sequence first");
+  if (num_blocks == 0 || num_tokens == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "pool_set: empty block summary cache");
+  if (!sums || !counts) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "pool_set: null summaries");
+  const uint64_t B = ctx->cfg.block_size;
+  if ((num_tokens + B - 1) / B != num_blocks)
+    return fail(ctx, HISA_ERR_SHAPE_MISMATCH, "pool_set: %llu tokens in blocks of %llu do not make %llu blocks",
+                (unsigned long long)num_tokens, (unsigned long long)B, (unsigned long long)num_blocks);
+  // blocks beyond the key sequence can never be eligible (t <= L - 1 after clipping): they are dropped
+  const uint32_t M = uint32_t(std::min<uint64_t>(num_blocks, num_blocks_of(ctx)));
+  const uint32_t d = ctx->cfg.dim;
+  const double* s_dev = sums;
+  const uint32_t* c_dev = counts;
+  if (!is_device_ptr(sums)) {
+    HISA_TRY(ensure(ctx, ctx->export_a, size_t(M) * d * sizeof(double)));
+    HISA_TRY(copy_in(ctx, ctx->export_a.p, sums, size_t(M) * d * sizeof(double)));
+    s_dev = ctx->export_a.as<double>();
+  }
+  if (!is_device_ptr(counts)) {
+    HISA_TRY(ensure(ctx, ctx->generic_n, size_t(M) * 4));
+    HISA_TRY(copy_in(ctx, ctx->generic_n.p, counts, size_t(M) * 4));
+    c_dev = ctx->generic_n.as<uint32_t>();
+  }
+  count_launches(ctx, launch_pool_import(s_dev, c_dev, M, d, ctx->cfg.pool_mode, ctx->sums.as<double>(),
+                                         ctx->counts.as<uint32_t>(), ctx->pooled_op.as<__nv_bfloat16>(), ctx->nseg_p,
+                                         ctx->stream));
+  HISA_TRY(check_launch(ctx, "pool import"));
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // the caller's host arrays may go away after the call
+  ctx->pool_external = true;
+  ctx->pool_blocks = M;
+  ctx->pooled_tokens = std::min<uint64_t>(num_tokens, ctx->seq_len);
+  return HISA_OK;
 }
 
 int hisa_cuda_pool_append(hisa_cuda_ctx* ctx, const void* keys, uint64_t n, uint32_t key_dim) {
@@ -1218,7 +1327,7 @@ int hisa_cuda_pool_read(hisa_cuda_ctx* ctx, double* sums, uint32_t* counts, doub
   CU_TRY(ctx, cudaSetDevice(ctx->device));
   if (ctx->seq_len == 0) return fail(ctx, HISA_ERR_EMPTY_SEQUENCE, "no block summaries: empty sequence");
   HISA_TRY(ensure_pool(ctx));
-  const uint32_t M = uint32_t(num_blocks_of(ctx)), d = ctx->cfg.dim;
+  const uint32_t M = uint32_t(pool_blocks_of(ctx)), d = ctx->cfg.dim;
   const size_t bytes = size_t(M) * d * sizeof(double);
   HISA_TRY(ensure(ctx, ctx->export_a, bytes));
   HISA_TRY(ensure(ctx, ctx->export_b, bytes));
@@ -1262,6 +1371,23 @@ int hisa_cuda_block_sparse_select(hisa_cuda_ctx* ctx, const void* queries, const
                      out_blocks, out_nblocks, nullptr);
 }
 
+int hisa_cuda_set_output_placement(hisa_cuda_ctx* ctx, const uint32_t* out_rows, int num_replicas,
+                                   int32_t* const* replica_idx, uint32_t* const* replica_count) {
+  if (!ctx) return fail(nullptr, HISA_ERR_INVALID_ARGUMENT, "null context");
+  if (num_replicas < 0 || num_replicas > kMaxReplicas)
+    return fail(ctx, HISA_ERR_UNSUPPORTED, "at most %d output replicas", kMaxReplicas);
+  if (num_replicas && !replica_idx) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "null replica list");
+  if (out_rows && !is_device_ptr(out_rows)) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "out_rows must be device memory");
+  ctx->place_rows = out_rows;
+  ctx->place_nrep = uint32_t(num_replicas);
+  for (int r = 0; r < kMaxReplicas; ++r) {
+    ctx->place_rep_idx[r] = r < num_replicas ? replica_idx[r] : nullptr;
+    ctx->place_rep_count[r] = (r < num_replicas && replica_count) ? replica_count[r] : nullptr;
+    if (r < num_replicas && !ctx->place_rep_idx[r]) return fail(ctx, HISA_ERR_INVALID_ARGUMENT, "null replica pointer");
+  }
+  return HISA_OK;
+}
+
 // ---- single stages ------------------------------------------------------------------------------------
 
 int hisa_cuda_score_blocks(hisa_cuda_ctx* ctx, const void* queries, const float* gates, const uint32_t* positions,
@@ -1276,7 +1402,7 @@ int hisa_cuda_score_blocks(hisa_cuda_ctx* ctx, const void* queries, const float*
   if (Q == 0) return HISA_OK;
   if (Q > uint64_t(ctx->chunk_dense) * 4096) return fail(ctx, HISA_ERR_UNSUPPORTED, "score_blocks: too many rows in one call");
   HISA_TRY(ensure(ctx, ctx->scalars, 64));
-  const uint32_t M = uint32_t(num_blocks_of(ctx)), Mpad = round_up(M, kTileRows);
+  const uint32_t M = uint32_t(pool_blocks_of(ctx)), Mpad = round_up(M, kTileRows);
   HISA_TRY(run_score_blocks(ctx, p, 0, Q, Mpad));
   if (out_scores)
     CU_TRY(ctx, cudaMemcpy2DAsync(out_scores, size_t(M) * 4, ctx->J.p, size_t(Mpad) * 4, size_t(M) * 4, Q,

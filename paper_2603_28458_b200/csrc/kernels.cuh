@@ -22,6 +22,7 @@ constexpr int kHeads = 64;      // heads per query in the operand (padded)
 constexpr int kDim = 128;       // elements per operand segment (padded d)
 constexpr int kGroupQ = 4;      // queries per MMA group (UMMA N = 256)
 constexpr int kMaxSeg = 3;
+constexpr int kMaxReplicas = 7;  // peer copies of the selection output (8-GPU box: 7 peers)
 
 // position of head j inside a query's 64-float gate row: heads {4i + c : i = 0..15} are the columns that
 // tcgen05.ld.16x128b hands to the lanes with (lane % 4) == c, and are stored as 16 consecutive floats.
@@ -113,6 +114,13 @@ struct SelectArgs {
   uint32_t out_width;  // entries to write per row (k, or m+2 for block modes)
   uint32_t* out_count;
   uint32_t* out_cand;
+  // output placement (multi-GPU row sharding): result row `row` of this launch is stored at row out_rows[row] of the
+  // output arrays (null = identity), and additionally at the same row of n_rep peer replicas of out_idx / out_count
+  // (device pointers, usually on OTHER GPUs with peer access enabled: the stores travel over NVLink)
+  const uint32_t* out_rows;
+  uint32_t n_rep;
+  int32_t* rep_out[kMaxReplicas];
+  uint32_t* rep_count[kMaxReplicas];
 };
 
 // sparse_attend / dense_attend (attention.hpp:48-59): one warp per query row
@@ -133,7 +141,13 @@ struct AttendArgs {
   uint32_t force_simt;    // HISA_ATTEND_SIMT: keep bf16 latents on the SIMT kernel (cross-check of the MMA kernel)
 };
 
-// ---- launchers (each returns the number of kernels it launched) ---------------------------------
+// Opts `func` into `bytes` of dynamic shared memory on the CURRENT device. The attribute belongs to the device's
+// context, not to the process, so the "already done" memo is keyed by (device, function): a process that drives one
+// hisa_cuda_ctx per GPU opts every kernel in on every device. Thread-safe. Returns false when the device refuses.
+bool smem_opt_in(const void* func, size_t bytes);
+
+// ---- launchers (each returns the number of kernels it launched; a negative value is a launch the device cannot
+// take, e.g. more shared memory than an SM has) -----------------------------------------------------------------
 // padded model dimension the attention kernel works on (32 * 2^i, at most 512); 0 = unsupported
 uint32_t attend_padded_dim(uint32_t d_model, bool bf16);
 int launch_sparse_attend(const AttendArgs& args, cudaStream_t stream);
@@ -157,7 +171,10 @@ int launch_build_dense_work(const uint32_t* pos, uint32_t nq, uint32_t chunk, ui
 int launch_invert_selection(const int32_t* sel, const uint32_t* nsel, uint32_t sel_stride, uint32_t nq,
                             uint32_t chunk, uint32_t num_blocks, uint32_t block_size, uint32_t segs_per_block,
                             uint32_t split, WorkItem* work, uint32_t* work_count, uint32_t* work_cursor, uint2* pairs,
-                            cudaStream_t stream);
+                            uint32_t* global_counters, cudaStream_t stream);
+// words of global scratch launch_invert_selection needs for its per-block counters (0: they fit in shared memory)
+size_t invert_global_words(uint32_t nq, uint32_t chunk, uint32_t num_blocks);
+size_t invert_smem_limit();
 // block-sparse output: tokens of the selected blocks clipped to <= t_eff
 int launch_expand_blocks(const int32_t* sel, const uint32_t* nsel, uint32_t sel_stride, const uint32_t* pos,
                          uint32_t nq, uint32_t seq_len, uint32_t block_size, int32_t* out_idx, uint64_t out_stride,
@@ -178,6 +195,10 @@ int launch_pool_update(const __nv_bfloat16* key_op, uint32_t nseg_k, uint64_t fi
 int launch_pool_update_fp8(const uint8_t* key8, const float* key_scale, uint64_t first, uint64_t n, uint32_t block_size,
                            uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op, uint32_t nseg_p,
                            cudaStream_t stream);
+// installs caller-provided summaries: src_sums f64 [num_blocks, dim], src_counts [num_blocks] (device pointers)
+int launch_pool_import(const double* src_sums, const uint32_t* src_counts, uint32_t num_blocks, uint32_t dim,
+                       uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op, uint32_t nseg_p,
+                       cudaStream_t stream);
 int launch_fill_f32(float* dst, uint64_t n, float v, cudaStream_t stream);
 int launch_pool_export(const double* sums, const uint32_t* counts, uint32_t num_blocks, uint32_t dim,
                        uint32_t pool_max, double* out_sums, double* out_pooled, cudaStream_t stream);

@@ -314,14 +314,7 @@ bool launch_pool_staged(const void* key_op, const float* key_scale, uint32_t nse
   const uint32_t row_bytes = FP8 ? uint32_t(kDim) : nseg_k * uint32_t(kDim) * 2u;
   const size_t smem = size_t(2) * kPoolChunkRows * row_bytes;
   auto kern = pool_update_staged_kernel<FP8>;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    configured = smem;
-  }
+  if (smem > 48 * 1024 && !smem_opt_in(reinterpret_cast<const void*>(kern), smem)) return false;
   const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
   kern<<<uint32_t(b1 - b0 + 1), kDim, smem, stream>>>(key_op, key_scale, nseg_k, first, n, block_size, pool_max, sums, counts,
                                                       pooled_op, nseg_p);
@@ -343,6 +336,23 @@ __global__ void pool_export_kernel(const double* __restrict__ sums, const uint32
   const double s = sums[uint64_t(b) * kDim + c];
   if (out_sums) out_sums[gid] = s;
   if (out_pooled) out_pooled[gid] = pool_max ? s : s / double(counts[b]);
+}
+
+// caller-provided summaries (BlockSummaryCache contents, block_summary.hpp:16-18): sums [M, dim] -> the context's padded
+// f64 sums, counts and the pooled operand, with the same sum / count -> f32 -> bf16 split as the pooling kernels
+__global__ void __launch_bounds__(kDim)
+pool_import_kernel(const double* __restrict__ src_sums, const uint32_t* __restrict__ src_counts, uint32_t dim,
+                   uint32_t pool_max, double* __restrict__ sums, uint32_t* __restrict__ counts,
+                   __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p) {
+  const uint32_t b = blockIdx.x, c = threadIdx.x;
+  const uint32_t cnt = src_counts[b];
+  const double s = c < dim ? src_sums[uint64_t(b) * dim + c] : 0.0;
+  sums[uint64_t(b) * kDim + c] = s;
+  if (c == 0) counts[b] = cnt;
+  const double p = pool_max ? s : (cnt ? s / double(cnt) : 0.0);
+  __nv_bfloat16 parts[kMaxSeg];
+  split_bf16(float(p), int(nseg_p), parts);
+  for (uint32_t g = 0; g < nseg_p; ++g) pooled_op[b * (uint64_t(nseg_p) * kDim) + g * kDim + c] = parts[g];
 }
 
 inline uint32_t blocks_for(uint64_t n, uint32_t threads) { return uint32_t((n + threads - 1) / threads); }
@@ -405,6 +415,14 @@ int launch_pool_update_fp8(const uint8_t* key8, const float* key_scale, uint64_t
   const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
   pool_update_fp8_kernel<<<uint32_t(b1 - b0 + 1), kDim, 0, stream>>>(key8, key_scale, first, n, block_size, pool_max, sums,
                                                                      counts, pooled_op, nseg_p);
+  return 1;
+}
+
+int launch_pool_import(const double* src_sums, const uint32_t* src_counts, uint32_t num_blocks, uint32_t dim,
+                       uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op, uint32_t nseg_p,
+                       cudaStream_t stream) {
+  if (num_blocks == 0) return 0;
+  pool_import_kernel<<<num_blocks, kDim, 0, stream>>>(src_sums, src_counts, dim, pool_max, sums, counts, pooled_op, nseg_p);
   return 1;
 }
 

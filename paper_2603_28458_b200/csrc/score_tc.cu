@@ -555,11 +555,7 @@ void launch_instance(const ScoreArgs& args, const CUtensorMap& map_a, const CUte
   using L = SmemLayout<NSEG_A, ABUF, NST, FP8 ? 1 : 2>;
   constexpr size_t smem = L::total + 1024;  // slack for the manual 1024 B alignment
   auto kern = score_tc_kernel<NSEG_A, NSEG_B, TERMS, ABUF, NST, FP8, STATS>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = true;
-  }
+  smem_opt_in(reinterpret_cast<const void*>(kern), smem);
   kern<<<num_sms, kTcThreads, smem, stream>>>(map_a, map_b, args);
 }
 

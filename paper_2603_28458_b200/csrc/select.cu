@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
     n = a.n_in[row];
   }
   const float* srow = a.scores + uint64_t(row) * a.stride;
-  int32_t* orow = a.out_idx + uint64_t(row) * a.out_stride;
+  const uint32_t orow_i = a.out_rows ? a.out_rows[row] : row;  // where this row's result lives in the output arrays
+  int32_t* orow = a.out_idx + uint64_t(orow_i) * a.out_stride;
   const uint32_t keep = a.keep;
   const bool forced = block_mode && a.force_first_last && n > 0;
 
@@ -132,12 +133,12 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
     return int32_t(i);
   };
 
-  if (a.out_cand && tid == 0) a.out_cand[row] = n;
+  if (a.out_cand && tid == 0) a.out_cand[orow_i] = n;
 
   // ---- everything fits: dense regime ------------------------------------
   if (n <= keep) {
     for (uint32_t i = tid; i < a.out_width; i += THREADS) orow[i] = i < n ? position_of(i) : -1;
-    if (a.out_count && tid == 0) a.out_count[row] = n;
+    if (a.out_count && tid == 0) a.out_count[orow_i] = n;
     return;
   }
 
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
   if (add_first && tid == 0) orow[0] = position_of(0);
   if (add_last && tid == 0) orow[count - 1] = position_of(n - 1);
   for (uint32_t i = count + tid; i < a.out_width; i += THREADS) orow[i] = -1;
-  if (a.out_count && tid == 0) a.out_count[row] = count;
+  if (a.out_count && tid == 0) a.out_count[orow_i] = count;
 }
 
 // ---------------------------------------------------------------------------------------------------
@@ -325,7 +326,8 @@ __global__ void __launch_bounds__(kWarpSelThreads) select_warp_kernel(SelectArgs
     n = a.n_in[row];
   }
   const float* srow = a.scores + uint64_t(row) * a.stride;
-  int32_t* orow = a.out_idx + uint64_t(row) * a.out_stride;
+  const uint32_t orow_i = a.out_rows ? a.out_rows[row] : row;  // where this row's result lives in the output arrays
+  int32_t* orow = a.out_idx + uint64_t(orow_i) * a.out_stride;
   const uint32_t keep = a.keep;
   const bool forced = block_mode && a.force_first_last && n > 0;
   const uint32_t bshift = a.block_shift;
@@ -336,10 +338,10 @@ __global__ void __launch_bounds__(kWarpSelThreads) select_warp_kernel(SelectArgs
     }
     return int32_t(i);
   };
-  if (a.out_cand && lane == 0) a.out_cand[row] = n;
+  if (a.out_cand && lane == 0) a.out_cand[orow_i] = n;
   if (n <= keep) {  // dense regime
     for (uint32_t i = lane; i < a.out_width; i += 32) orow[i] = i < n ? position_of(i) : -1;
-    if (a.out_count && lane == 0) a.out_count[row] = n;
+    if (a.out_count && lane == 0) a.out_count[orow_i] = n;
     return;
   }
   const bool boost = forced && a.forced_in_budget;
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(kWarpSelThreads) select_warp_kernel(SelectArgs
   if (lane == 0) {
     if (add_first) orow[0] = position_of(0);
     if (add_last) orow[count - 1] = position_of(n - 1);
-    if (a.out_count) a.out_count[row] = count;
+    if (a.out_count) a.out_count[orow_i] = count;
   }
   for (uint32_t i = count + lane; i < a.out_width; i += 32) orow[i] = -1;
 }
@@ -503,7 +505,8 @@ __global__ void __launch_bounds__(THREADS) select_cta_kernel(SelectArgs a) {
     n = a.n_in[row];
   }
   const float* srow = a.scores + uint64_t(row) * a.stride;
-  int32_t* orow = a.out_idx + uint64_t(row) * a.out_stride;
+  const uint32_t orow_i = a.out_rows ? a.out_rows[row] : row;  // where this row's result lives in the output arrays
+  int32_t* orow = a.out_idx + uint64_t(orow_i) * a.out_stride;
   const uint32_t keep = a.keep;
   const bool forced = block_mode && a.force_first_last && n > 0;
   const uint32_t bshift = a.block_shift;
@@ -514,7 +517,7 @@ __global__ void __launch_bounds__(THREADS) select_cta_kernel(SelectArgs a) {
     }
     return int32_t(i);
   };
-  if (a.out_cand && tid == 0) a.out_cand[row] = n;
+  if (a.out_cand && tid == 0) a.out_cand[orow_i] = n;
 
   const bool dense = n <= keep;
   const uint32_t n4 = (n + 3u) >> 2;  // 16-byte chunks that hold candidates
@@ -535,7 +538,7 @@ __global__ void __launch_bounds__(THREADS) select_cta_kernel(SelectArgs a) {
 
   if (dense) {  // everything fits
     for (uint32_t i = tid; i < a.out_width; i += THREADS) orow[i] = i < n ? position_of(i) : -1;
-    if (a.out_count && tid == 0) a.out_count[row] = n;
+    if (a.out_count && tid == 0) a.out_count[orow_i] = n;
     return;
   }
   mbar_wait(&bar, 0);
@@ -731,7 +734,7 @@ __global__ void __launch_bounds__(THREADS) select_cta_kernel(SelectArgs a) {
   if (tid == 0) {
     if (add_first) put(0, position_of(0));
     if (add_last) put(count - 1, position_of(n - 1));
-    if (a.out_count) a.out_count[row] = count;
+    if (a.out_count) a.out_count[orow_i] = count;
   }
   if (staged) {
     __syncthreads();
@@ -839,7 +842,8 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
     n = a.n_in[row];
   }
   const float* srow = a.scores + uint64_t(row) * a.stride;
-  int32_t* orow = a.out_idx + uint64_t(row) * a.out_stride;
+  const uint32_t orow_i = a.out_rows ? a.out_rows[row] : row;  // where this row's result lives in the output arrays
+  int32_t* orow = a.out_idx + uint64_t(orow_i) * a.out_stride;
   const uint32_t keep = a.keep;
   const uint32_t bshift = a.block_shift;
   auto position_of = [&](uint32_t i) -> int32_t {
@@ -849,7 +853,7 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
     }
     return int32_t(i);
   };
-  if (a.out_cand && tid == 0) a.out_cand[row] = n;
+  if (a.out_cand && tid == 0) a.out_cand[orow_i] = n;
 
   const bool dense = n <= keep;
   const uint32_t n4 = (n + 3u) >> 2;  // 16-byte chunks that hold candidates
@@ -870,8 +874,16 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
   __syncthreads();
 
   if (dense) {  // everything fits
-    for (uint32_t i = tid; i < a.out_width; i += THREADS) orow[i] = i < n ? position_of(i) : -1;
-    if (a.out_count && tid == 0) a.out_count[row] = n;
+    for (uint32_t i = tid; i < a.out_width; i += THREADS) {
+      const int32_t v = i < n ? position_of(i) : -1;
+      orow[i] = v;
+      for (uint32_t r = 0; r < a.n_rep; ++r) a.rep_out[r][uint64_t(orow_i) * a.out_stride + i] = v;
+    }
+    if (tid == 0) {
+      if (a.out_count) a.out_count[orow_i] = n;
+      for (uint32_t r = 0; r < a.n_rep; ++r)
+        if (a.rep_count[r]) a.rep_count[r][orow_i] = n;
+    }
     return;
   }
   mbar_wait(&bar, 0);
@@ -1096,7 +1108,10 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
       emit(first + 32 + e);
     }
   }
-  if (tid == 0 && a.out_count) a.out_count[row] = count;
+  if (tid == 0 && a.out_count) a.out_count[orow_i] = count;
+  if (tid == 0)
+    for (uint32_t r = 0; r < a.n_rep; ++r)
+      if (a.rep_count[r]) a.rep_count[r][orow_i] = count;
   if (staged) {
     __syncthreads();
     if (a.vec_out) {
@@ -1113,6 +1128,10 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
           v.w = i0 + 3 < count ? int32_t(hist[i0 + 3]) : -1;
         }
         reinterpret_cast<int4*>(orow)[c] = v;
+        // fused all-gather: the same 16 bytes go to the row's place in every peer GPU's [Q, k] matrix (NVLink stores
+        // to peer memory), so the selection kernel IS the collective and no staging copy or permutation follows it
+        for (uint32_t r = 0; r < a.n_rep; ++r)
+          reinterpret_cast<int4*>(a.rep_out[r] + uint64_t(orow_i) * a.out_stride)[c] = v;
       }
       for (uint32_t i = (w4 << 2) + tid; i < a.out_width; i += THREADS) orow[i] = i < count ? int32_t(hist[i]) : -1;
     } else {
@@ -1187,12 +1206,14 @@ __global__ void __launch_bounds__(kInvThreads)
 invert_selection_kernel(const int32_t* __restrict__ sel, const uint32_t* __restrict__ nsel, uint32_t sel_stride,
                         uint32_t nq, uint32_t chunk, uint32_t num_blocks, uint32_t block_size,
                         uint32_t segs_per_block, uint32_t split, WorkItem* __restrict__ work,
-                        uint32_t* __restrict__ work_count, uint2* __restrict__ pairs) {
+                        uint32_t* __restrict__ work_count, uint2* __restrict__ pairs, uint32_t* __restrict__ gcount) {
   extern __shared__ __align__(16) uint32_t smem_u[];
-  uint32_t* cnt = smem_u;                  // [num_blocks]
-  uint32_t* off = smem_u + num_blocks;     // [num_blocks]
-  uint32_t* scratch = off + num_blocks;    // [64]
+  // per-block counters live in shared memory; sequences with more blocks than fit there (gcount != null: 1M tokens at
+  // B = 32, or the degenerate B = 1) keep them in a per-chunk slice of global memory instead
   const uint32_t c = blockIdx.x, tid = threadIdx.x;
+  uint32_t* cnt = gcount ? gcount + uint64_t(c) * 2u * num_blocks : smem_u + 64;  // [num_blocks]
+  uint32_t* off = cnt + num_blocks;                                               // [num_blocks]
+  uint32_t* scratch = smem_u;                                                     // [64]
   const uint32_t q0 = c * chunk, q1 = min(nq, q0 + chunk);
   for (uint32_t b = tid; b < num_blocks; b += kInvThreads) cnt[b] = 0;
   __syncthreads();
@@ -1244,6 +1265,24 @@ invert_selection_kernel(const int32_t* __restrict__ sel, const uint32_t* __restr
   }
 }
 
+// Copies finished result rows to the peer replicas (variants that do not store to the peers themselves). One CTA per row.
+__global__ void __launch_bounds__(256) replicate_rows_kernel(SelectArgs a) {
+  const uint32_t row = blockIdx.x;
+  const uint32_t orow_i = a.out_rows ? a.out_rows[row] : row;
+  const int32_t* src = a.out_idx + uint64_t(orow_i) * a.out_stride;
+  for (uint32_t r = 0; r < a.n_rep; ++r) {
+    int32_t* dst = a.rep_out[r] + uint64_t(orow_i) * a.out_stride;
+    if (a.vec_out) {
+      for (uint32_t c = threadIdx.x; c < (a.out_width >> 2); c += blockDim.x)
+        reinterpret_cast<int4*>(dst)[c] = reinterpret_cast<const int4*>(src)[c];
+      for (uint32_t i = (a.out_width & ~3u) + threadIdx.x; i < a.out_width; i += blockDim.x) dst[i] = src[i];
+    } else {
+      for (uint32_t i = threadIdx.x; i < a.out_width; i += blockDim.x) dst[i] = src[i];
+    }
+    if (threadIdx.x == 0 && a.rep_count[r] && a.out_count) a.rep_count[r][orow_i] = a.out_count[orow_i];
+  }
+}
+
 __global__ void zero_two_kernel(uint32_t* a, uint32_t* b) {
   *a = 0;
   *b = 0;
@@ -1259,11 +1298,7 @@ template <int THREADS, int PER4>
 void launch_select_cta(const SelectArgs& args, uint32_t rows, cudaStream_t stream) {
   const size_t smem = (size_t(THREADS) * PER4 * 4 + kBins + kListCap + args.sel_stride + 96) * sizeof(uint32_t);
   auto kern = select_cta_kernel<THREADS, PER4>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
+  smem_opt_in(reinterpret_cast<const void*>(kern), 200 * 1024);
   kern<<<rows, THREADS, smem, stream>>>(args);
 }
 
@@ -1271,11 +1306,7 @@ template <int THREADS, int PER4>
 void launch_select_tok(const SelectArgs& args, uint32_t rows, cudaStream_t stream) {
   const size_t smem = (size_t(THREADS) * PER4 * 4 + kBins + THREADS + args.sel_stride + 96) * sizeof(uint32_t);
   auto kern = select_tok_kernel<THREADS, PER4>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
+  smem_opt_in(reinterpret_cast<const void*>(kern), 200 * 1024);
   kern<<<rows, THREADS, smem, stream>>>(args);
 }
 
@@ -1283,7 +1314,7 @@ template <int THREADS, bool SMEM_KEYS>
 void launch_select_variant(const SelectArgs& args, uint32_t rows, uint32_t n_cap, cudaStream_t stream) {
   const size_t smem = (size_t(kBins) + 64 + kListCap + args.sel_stride + (SMEM_KEYS ? n_cap : 0)) * sizeof(uint32_t);
   auto kern = select_rows_kernel<THREADS, SMEM_KEYS>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (smem > 48 * 1024) smem_opt_in(reinterpret_cast<const void*>(kern), smem);
   kern<<<rows, THREADS, smem, stream>>>(args);
 }
 
@@ -1303,11 +1334,12 @@ int launch_select(const SelectArgs& args_in, uint32_t rows, uint32_t n_cap, cuda
   const bool block_mode = args.mode == kSelBlocks || args.mode == kSelBlocksGeneric;
   // bulk-copy path: 16-byte aligned rows whose stride covers the rounded-up chunk count
   const bool bulk_ok = args.vec_ok && args.scores != nullptr;
+  bool fused_rep = false;  // the variant stores to the peer replicas itself
   if (!legacy && n_cap <= 128) launch_select_warp<4>(args, rows, stream);
   else if (!legacy && n_cap <= 512) launch_select_warp<16>(args, rows, stream);
   else if (!legacy && n_cap <= 1024) launch_select_warp<32>(args, rows, stream);
-  else if (!legacy && bulk_ok && !block_mode && !cta_old && n_cap <= 256 * 9 * 4) launch_select_tok<256, 9>(args, rows, stream);
-  else if (!legacy && bulk_ok && !block_mode && !cta_old && n_cap <= 512 * 9 * 4) launch_select_tok<512, 9>(args, rows, stream);
+  else if (!legacy && bulk_ok && !block_mode && !cta_old && n_cap <= 256 * 9 * 4) { launch_select_tok<256, 9>(args, rows, stream); fused_rep = args.vec_out && args.keep <= uint32_t(kBins); }
+  else if (!legacy && bulk_ok && !block_mode && !cta_old && n_cap <= 512 * 9 * 4) { launch_select_tok<512, 9>(args, rows, stream); fused_rep = args.vec_out && args.keep <= uint32_t(kBins); }
   else if (!legacy && bulk_ok && n_cap <= 256 * 9 * 4) launch_select_cta<256, 9>(args, rows, stream);
   else if (!legacy && bulk_ok && n_cap <= 512 * 9 * 4) launch_select_cta<512, 9>(args, rows, stream);
   else if (!legacy && bulk_ok && n_cap <= 1024 * 9 * 4) launch_select_cta<1024, 9>(args, rows, stream);
@@ -1315,7 +1347,10 @@ int launch_select(const SelectArgs& args_in, uint32_t rows, uint32_t n_cap, cuda
   else if (n_cap <= 16384) launch_select_variant<256, true>(args, rows, n_cap, stream);
   else if (n_cap <= 49152) launch_select_variant<1024, true>(args, rows, n_cap, stream);
   else launch_select_variant<1024, false>(args, rows, n_cap, stream);
-  return 1;
+  if (args.n_rep == 0) return 1;
+  if (fused_rep) return 1;
+  replicate_rows_kernel<<<rows, 256, 0, stream>>>(args);
+  return 2;
 }
 
 int launch_build_dense_work(const uint32_t* pos, uint32_t nq, uint32_t chunk, uint32_t seq_len, uint32_t unit_div,
@@ -1329,17 +1364,30 @@ int launch_build_dense_work(const uint32_t* pos, uint32_t nq, uint32_t chunk, ui
 
 int launch_invert_selection(const int32_t* sel, const uint32_t* nsel, uint32_t sel_stride, uint32_t nq, uint32_t chunk,
                             uint32_t num_blocks, uint32_t block_size, uint32_t segs_per_block, uint32_t split,
-                            WorkItem* work, uint32_t* work_count, uint32_t* work_cursor, uint2* pairs, cudaStream_t stream) {
+                            WorkItem* work, uint32_t* work_count, uint32_t* work_cursor, uint2* pairs,
+                            uint32_t* global_counters, cudaStream_t stream) {
   if (nq == 0) return 0;
   zero_two_kernel<<<1, 1, 0, stream>>>(work_count, work_cursor);
-  const size_t smem = (size_t(num_blocks) * 2 + 64) * sizeof(uint32_t);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(invert_selection_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  size_t smem = (size_t(num_blocks) * 2 + 64) * sizeof(uint32_t);
+  uint32_t* gcount = nullptr;
+  if (smem > invert_smem_limit()) {
+    if (!global_counters) return -1;  // the caller sizes the scratch with invert_global_words()
+    gcount = global_counters;
+    smem = 64 * sizeof(uint32_t);
+  } else if (smem > 48 * 1024 && !smem_opt_in(reinterpret_cast<const void*>(invert_selection_kernel), smem)) {
+    return -1;
+  }
   const uint32_t nchunks = (nq + chunk - 1) / chunk;
   invert_selection_kernel<<<nchunks, kInvThreads, smem, stream>>>(sel, nsel, sel_stride, nq, chunk, num_blocks,
                                                                   block_size, segs_per_block, split ? split : 0xFFFFFFFFu, work,
-                                                                  work_count, pairs);
+                                                                  work_count, pairs, gcount);
   return 2;
+}
+
+size_t invert_smem_limit() { return 200 * 1024; }
+size_t invert_global_words(uint32_t nq, uint32_t chunk, uint32_t num_blocks) {
+  if ((size_t(num_blocks) * 2 + 64) * sizeof(uint32_t) <= invert_smem_limit()) return 0;
+  return size_t((nq + chunk - 1) / chunk) * 2u * num_blocks;
 }
 
 int launch_expand_blocks(const int32_t* sel, const uint32_t* nsel, uint32_t sel_stride, const uint32_t* pos,

@@ -57,3 +57,36 @@ def test_dropin_spec_examples_on_gpu(built):
     print(r.stdout[-3000:], r.stderr[-2000:])
     assert r.returncode == 0, r.stdout[-3000:]
     assert "PASSED" in r.stdout
+
+
+# ---- boundary fidelity: the C++ layer is written against the reference's OWN headers --------------------------------
+REF_INC = "/root/reference/proj/core/include"
+CPP_DIR = os.path.join(ROOT, "paper_2603_28458_b200", "cpp")
+TUS = ["hisa_gpu.cpp", "hisa_consumer.cpp", "hisa_niah.cpp", "hisa_multi.cpp", "test_dropin.cpp", "test_host.cpp"]
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(REF_INC, "hisa")), reason="reference tree not present (GPU box)")
+@pytest.mark.parametrize("tu", TUS)
+def test_translation_units_compile_against_the_reference_headers(tu):
+    """Every translation unit of the drop-in (and its callers' test programs) compiles with the reference's
+    proj/core/include AHEAD of this repository's include/: all hisa::* declarations come from the reference, only
+    hisa_gpu.hpp (namespace hisa::gpu) and hisa_cuda.h (the C ABI) come from here."""
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-Werror", "-M", f"-I{REF_INC}",
+                        f"-I{os.path.join(ROOT, 'include')}", os.path.join(CPP_DIR, tu)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-4000:]
+    deps = r.stdout.replace("\\\n", " ").split()
+    ours = [d for d in deps if os.path.abspath(d).startswith(os.path.join(ROOT, "include") + os.sep)]
+    assert set(os.path.basename(d) for d in ours) <= {"hisa_cuda.h", "hisa_gpu.hpp"}, ours
+    assert any(d.startswith(REF_INC) for d in deps), "no reference header was used"
+    # and the same unit really compiles (not only preprocesses) in that configuration
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-Werror", f"-I{REF_INC}",
+                        f"-I{os.path.join(ROOT, 'include')}", os.path.join(CPP_DIR, tu)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("tu", TUS)
+def test_translation_units_compile_against_the_stand_in_headers(tu):
+    """Without the reference tree (the GPU box), include/hisa/*.hpp restate the same declarations."""
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-Werror",
+                        f"-I{os.path.join(ROOT, 'include')}", os.path.join(CPP_DIR, tu)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-4000:]
