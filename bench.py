@@ -46,7 +46,10 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--force-dist", action="store_true",
-                    help="initialise NCCL even with one rank (exercises the multi-GPU code path on a single GPU)")
+                    help="use the multi-GPU driver (hisa_cuda_dist_*, NCCL communicator) even with one rank")
+    ap.add_argument("--no-configs", action="store_true", help="skip the array of the other BASELINE configurations")
+    ap.add_argument("--configs-only", default="", help="comma list of configuration ids to time (default: all)")
+    ap.add_argument("--slices", type=int, default=0, help="slices per rank of the sharded step (0 = 4, or 2 for short ranks)")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp8"],
                     help="storage of q/k: bf16 (headline) or e4m3 with per-token key scales (query scales folded into the gates)")
     return ap.parse_args()
@@ -117,7 +120,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------- sharding
-from paper_2603_28458_b200.sharding import TILE_ROWS, rank_rows  # noqa: E402  (query tiles dealt zig-zag over ranks)
+TILE_ROWS = 512  # hisa_cuda.h: HISA_DIST_TILE_ROWS (the plan itself comes from the C library: capi.dist_plan)
 
 
 # ------------------------------------------------------------------------------------------- reference arm
@@ -202,6 +205,179 @@ def run_consumer_leg(a, capi, ix, torch, dev, g, step_hisa, L, nq, k, pos, out_i
     return consumer
 
 
+
+# ------------------------------------------------------------------------------------------- the other BASELINE configs
+def measure_config(torch, capi, dev, peaks, cid, name, L, rows, B, m, k, dtype="bf16", steps=3, warmup=1, flat_steps=1,
+                   decode=False):
+    """One BASELINE.json configuration through the C ABI on one GPU: device-resident synthetic inputs, CUDA events on the
+    context's stream, per-stage events. decode=True: every step first appends ONE key (BlockSummaryCache::append,
+    block_summary.hpp:27-30) and all queries sit at the newest position. Returns a dict for the `configs` array."""
+    H, d = 64, 128
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    rows = np.asarray(rows, dtype=np.int64)
+    nq = len(rows)
+    cap = L + (steps + warmup + 16 if decode else 0)
+    keys_f = torch.randn((cap, d), generator=g, device=dev, dtype=torch.float32)
+    scales = None
+    if dtype == "fp8":
+        scales = (keys_f.abs().amax(dim=1) / 448.0).clamp_min(1e-12).contiguous()
+        keys = (keys_f / scales[:, None]).to(torch.float8_e4m3fn)
+        code = capi.DTYPE_FP8
+    elif dtype == "f32":
+        keys, code = keys_f, capi.DTYPE_F32
+    else:
+        keys, code = keys_f.to(torch.bfloat16), capi.DTYPE_BF16
+    del keys_f
+    w = torch.rand((nq, H), generator=g, device=dev, dtype=torch.float32) + 0.5
+    if dtype == "fp8":
+        q = torch.empty((nq, H, d), device=dev, dtype=torch.float8_e4m3fn)
+        for r0 in range(0, nq, 8192):
+            qf = torch.randn((min(8192, nq - r0), H, d), generator=g, device=dev, dtype=torch.float32)
+            qs = (qf.abs().amax(dim=2) / 448.0).clamp_min(1e-12)
+            q[r0:r0 + qf.shape[0]] = (qf / qs[:, :, None]).to(torch.float8_e4m3fn)
+            w[r0:r0 + qf.shape[0]] *= qs
+    else:
+        q = torch.empty((nq, H, d), device=dev, dtype=torch.float32 if dtype == "f32" else torch.bfloat16)
+        for r0 in range(0, nq, 16384):
+            q[r0:r0 + 16384] = torch.randn((min(16384, nq - r0), H, d), generator=g, device=dev, dtype=torch.float32).to(q.dtype)
+    pos = torch.from_numpy(rows).to(dev).to(torch.int32)
+    out_idx = torch.empty((nq, k), device=dev, dtype=torch.int32)
+    out_count = torch.empty((nq,), device=dev, dtype=torch.int32)
+    out_cand = torch.empty((nq,), device=dev, dtype=torch.int32)
+    torch.cuda.synchronize()
+    eb = q.element_size()
+    cfg = capi.make_config(B, m, k, H, d, code)
+    with capi.Indexer(cfg, dev.index or 0) as ix, ClockSampler(dev.index or 0) as clocks:
+        ix.upload_keys(keys.data_ptr(), seq_len=L, scales=scales.data_ptr() if scales is not None else None)
+        ix.pool_build()
+        ix.synchronize()
+        stream = torch.cuda.ExternalStream(capi.lib().hisa_cuda_stream(ix._ctx), device=dev)
+        state = {"L": L}
+
+        def step_hisa():
+            if decode:
+                at = state["L"]
+                ix.pool_append(keys.data_ptr() + at * d * eb, n=1, key_dim=d,
+                               scales=(scales.data_ptr() + at * 4) if scales is not None else None)
+                state["L"] += 1
+                with torch.cuda.stream(stream):
+                    pos.fill_(state["L"] - 1)
+            ix.hisa_select_raw(q.data_ptr(), w.data_ptr(), pos.data_ptr(), nq, out_idx.data_ptr(), out_count.data_ptr(),
+                               None, None, out_cand.data_ptr())
+
+        def step_flat():
+            ix.dsa_select_raw(q.data_ptr(), w.data_ptr(), pos.data_ptr(), nq, out_idx.data_ptr(), out_count.data_ptr(), None)
+
+        def run(fn, n, wu, profile):
+            for _ in range(wu):
+                fn()
+            ix.synchronize()
+            if profile:
+                ix.set_profiling(True)
+                ix.stage_times()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record()
+            t0 = time.perf_counter()
+            for _ in range(n):
+                fn()
+            host_s = time.perf_counter() - t0
+            with torch.cuda.stream(stream):
+                e1.record()
+            ix.synchronize()
+            st = ix.stage_times() if profile else None
+            if profile:
+                ix.set_profiling(False)
+            return e0.elapsed_time(e1) / n, st, host_s / n
+
+        # decode steps are a handful of short kernels: stage events would be a large part of what they measure, so the
+        # step is timed without them first and the per-stage split comes from a second, separately profiled pass
+        ms, _, host_s = run(step_hisa, steps, warmup, profile=False)
+        _, st, _ = run(step_hisa, max(1, min(steps, 5)), 0, profile=True)
+        calls = max(st["calls"], 1)
+        stages = {kk: vv / calls for kk, vv in st.items() if kk.endswith("_ms")}
+        cand = int(out_cand.to(torch.int64).sum().item())
+        pos64 = pos.to(torch.int64).clamp(max=state["L"] - 1)
+        elig = int((pos64 // B + 1).sum().item())
+        prefix = int((pos64 + 1).sum().item())
+        flat_ms = flat_st = None
+        if flat_steps:
+            flat_ms, flat_st, _ = run(step_flat, flat_steps, 1, profile=True)
+        tpeak = peaks["tflops"]
+        if dtype == "fp8":
+            fpath = os.path.join(ROOT, "profiles", "fp8_peak.json")
+            tpeak = float(json.load(open(fpath))["fp8_tflops_sustained"]) if os.path.exists(fpath) else 2.0 * tpeak
+
+        def frac(work, ms_, peak, scale):
+            return round(work / (ms_ * 1e-3) / scale / peak, 4) if ms_ and ms_ > 0 else None
+        out = {
+            "id": cid, "workload": name, "dtype": dtype, "L": L, "Q": nq, "B": B, "m": m, "k": k,
+            "ms_per_step": round(ms, 4), "queries_per_s": round(nq / (ms * 1e-3), 1),
+            "stages_ms": {kk: round(vv, 4) for kk, vv in stages.items()},
+            "launches_per_step": st["launches"] // calls,
+            "host_enqueue_us_per_step": round(host_s * 1e6, 1),
+            "roofline_frac": {
+                "score_blocks (tensor, algorithmic)": frac(2.0 * d * H * elig, stages["score_blocks_ms"], peaks["tflops"], 1e12),
+                "score_tokens (tensor)": frac(2.0 * d * H * cand, stages["score_tokens_ms"], tpeak, 1e12),
+                "top_k (hbm)": frac(4.0 * cand + 4.0 * nq * k, stages["top_k_ms"], peaks["hbm_gbs"], 1e9),
+                "select_blocks (hbm)": frac(4.0 * elig + 4.0 * nq * (m + 2), stages["select_blocks_ms"], peaks["hbm_gbs"], 1e9),
+            },
+            "stage2_tflops": round(2.0 * d * H * cand / (stages["score_tokens_ms"] * 1e-3) / 1e12, 1) if stages["score_tokens_ms"] > 0 else None,
+            "flat_dsa": None,
+            "clocks": clocks.summary(),
+        }
+        if flat_ms:
+            fcalls = max(flat_st["calls"], 1)
+            fk = flat_st["score_tokens_ms"] / fcalls
+            out["flat_dsa"] = {"ms_per_step": round(flat_ms, 4), "scorer_ms": round(fk, 4),
+                               "top_k_ms": round(flat_st["top_k_ms"] / fcalls, 4),
+                               "scorer_tflops": round(2.0 * d * H * prefix / (fk * 1e-3) / 1e12, 1) if fk > 0 else None,
+                               "hisa_speedup": round(flat_ms / ms, 3),
+                               "hisa_speedup_scorers_only": round(fk / stages["score_tokens_ms"], 3) if stages["score_tokens_ms"] > 0 else None,
+                               "flop_ratio_flat_over_hisa": round(prefix / max(cand + elig, 1), 3)}
+    del q, w, keys, out_idx
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_configs(a, torch, capi, dev, peaks):
+    """Every BASELINE.json configuration other than the headline one (which is the line itself), bounded to about a minute
+    in total. Parity of these shapes is the job of tests/ (-m gpu); here they are timed."""
+    table = [
+        # id, name, L, rows, B, m, k, dtype, steps, warmup, flat_steps, decode
+        ("C1", "CPU-reference shape: prefill L=Q=8192, m=32, f32 storage (3x3 bf16 split, 6 MMA terms)", 8192,
+         np.arange(8192), 128, 32, 2048, "f32", 5, 2, 2, False),
+        ("C2", "DeepSeek-V3.2 indexer shape: prefill L=Q=32768, bf16", 32768, np.arange(32768), 128, 64, 2048, "bf16", 5, 2, 2, False),
+        ("C3-fp8", "headline shape with e4m3 q/k + per-key f32 scales", 65536, np.arange(65536), 128, 64, 2048, "fp8", 5, 2, 1, False),
+        ("C3-paper", "the paper's measurement shape (PAPER.md:257): last 1024 query rows of a 64K context", 65536,
+         np.arange(65536 - 1024, 65536), 128, 64, 2048, "bf16", 20, 3, 5, False),
+        ("C3-4to1", "Fig. 2 panel b (PAPER.md:192,261): M:m = 4:1 at 64K, m=128 (16.6K candidates)", 65536, np.arange(65536),
+         128, 128, 2048, "bf16", 3, 1, 0, False),
+        ("C3-4to1-paper", "same, the paper's 1024-row tail", 65536, np.arange(65536 - 1024, 65536), 128, 128, 2048, "bf16", 20, 3, 5, False),
+        ("C4", "prefill L=Q=131072 on ONE GPU (the sharded configuration's single-GPU leg)", 131072, np.arange(131072),
+         128, 64, 2048, "bf16", 2, 1, 1, False),
+        ("C5-128K", "decode: 64 queries at the newest position of a 128K prefix, +1 key appended per step", 131072,
+         np.full(64, 131071), 128, 64, 2048, "bf16", 100, 10, 10, True),
+        ("C5-1M", "decode: 64 queries at the newest position of a 1M prefix, +1 key appended per step", 1048576,
+         np.full(64, 1048575), 128, 64, 2048, "bf16", 100, 10, 5, True),
+    ]
+    only = [c for c in a.configs_only.split(",") if c]
+    out = []
+    t_start = time.perf_counter()
+    for cid, name, L, rows, B, m, k, dt, steps, wu, fsteps, dec in table:
+        if only and cid not in only:
+            continue
+        if not only and time.perf_counter() - t_start > 75.0:
+            out.append({"id": cid, "skipped": "time budget of the configs array spent"})
+            continue
+        try:
+            out.append(measure_config(torch, capi, dev, peaks, cid, name, L, rows, B, m, k, dt, steps, wu, fsteps, dec))
+        except Exception as exc:  # an extra: never lose the headline line over it
+            out.append({"id": cid, "error": f"{type(exc).__name__}: {exc}"})
+    return out
+
+
 # ------------------------------------------------------------------------------------------- B200 arm
 def run_b200(a, rank, world, local_rank):
     import torch
@@ -209,10 +385,16 @@ def run_b200(a, rank, world, local_rank):
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device — the product path has no CPU fallback")
+    if world > torch.cuda.device_count() and "LOCAL_RANK" in os.environ:
+        raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} CUDA device(s) on this node")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    # torch.distributed is launcher plumbing only (rendezvous, barrier, max over ranks of the timings, and carrying the
+    # 128-byte NCCL id to the ranks); every byte of the data path — key replication, selection, the gather of the index
+    # rows — goes through the C ABI's multi-GPU driver (hisa_cuda_dist_*: its own NCCL communicator, its own streams)
     dist = None
-    if world > 1 or a.force_dist:
+    use_driver = world > 1 or a.force_dist
+    if world > 1:
         import torch.distributed as dist_mod
         dist = dist_mod
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -223,21 +405,18 @@ def run_b200(a, rank, world, local_rank):
     H, d, B, m, k = 64, 128, a.block_size, a.block_budget, a.token_budget
     g = torch.Generator(device=dev)
     g.manual_seed(a.seed)
-    # keys: generated on rank 0 and replicated (NCCL broadcast over NVLink); queries: each rank generates only
-    # the rows it owns (synthetic, so nothing has to be scattered)
     fp8 = a.dtype == "fp8"
-    keys = torch.randn((L, d), generator=g, device=dev, dtype=torch.float32)
-    key_scales = None
-    if fp8:  # per-token symmetric quantisation (synthetic-input plumbing; the product consumes bytes + scales)
-        key_scales = (keys.abs().amax(dim=1) / 448.0).clamp_min(1e-12).contiguous()
-        keys = (keys / key_scales[:, None]).to(torch.float8_e4m3fn)
-    else:
-        keys = keys.to(torch.bfloat16)
-    if dist:
-        dist.broadcast(keys.view(torch.uint8) if fp8 else keys, src=0)
-        if fp8:
-            dist.broadcast(key_scales, src=0)
-    rows = rank_rows(Q, world, rank)
+    # keys exist on rank 0 only (the other ranks receive them by ncclBroadcast inside the driver); queries: each rank
+    # generates only the rows it owns (synthetic, so nothing has to be scattered)
+    keys = key_scales = None
+    if rank == 0:
+        keys = torch.randn((L, d), generator=g, device=dev, dtype=torch.float32)
+        if fp8:  # per-token symmetric quantisation (synthetic-input plumbing; the product consumes bytes + scales)
+            key_scales = (keys.abs().amax(dim=1) / 448.0).clamp_min(1e-12).contiguous()
+            keys = (keys / key_scales[:, None]).to(torch.float8_e4m3fn)
+        else:
+            keys = keys.to(torch.bfloat16)
+    rows = capi.dist_plan(Q, world, rank)  # the C library's own sharding plan: 512-row tiles, zig-zag over the ranks
     nq = len(rows)
     g.manual_seed(a.seed + 1000 + rank)
     w = torch.rand((nq, H), generator=g, device=dev, dtype=torch.float32) + 0.5
@@ -255,21 +434,28 @@ def run_b200(a, rank, world, local_rank):
     out_idx = torch.empty((nq, k), device=dev, dtype=torch.int32)
     out_count = torch.empty((nq,), device=dev, dtype=torch.int32)
     out_cand = torch.empty((nq,), device=dev, dtype=torch.int32)
-    # multi-GPU: the rank's rows are selected in slices, and the all-gather of slice i (NCCL, its own stream) runs
-    # under the kernels of slice i+1 — at 8 GPUs the gather of the indices costs about half of the per-rank compute
-    # (SURVEY.md §8e), so it must not be serialised behind it
-    n_slices = 1 if not dist else (4 if nq > 8192 else 2)
-    step_rows = -(-nq // (n_slices * TILE_ROWS)) * TILE_ROWS
-    bounds = [min(i * step_rows, nq) for i in range(n_slices + 1)]
-    gathered = [torch.empty((world * (bounds[i + 1] - bounds[i]), k), device=dev, dtype=torch.int32)
-                for i in range(n_slices)] if dist else None
-    comm_stream = torch.cuda.Stream(device=dev) if dist else None
-    slice_done = [torch.cuda.Event() for _ in range(n_slices)] if dist else None
     torch.cuda.synchronize()
 
     cfg = capi.make_config(B, m, k, H, d, capi.DTYPE_FP8 if fp8 else capi.DTYPE_BF16)
-    ix = capi.Indexer(cfg, local_rank)
-    ix.upload_keys(keys.data_ptr(), seq_len=L, scales=key_scales.data_ptr() if fp8 else None)
+    driver = None
+    n_slices = 1
+    if use_driver:
+        # one rank per process (the launcher's model): rank 0 makes the NCCL id, torch carries it to the others
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(capi.dist_unique_id()), dtype=torch.uint8))
+        if dist:
+            dist.broadcast(uid, src=0)
+        driver = capi.Dist(cfg, rank=rank, world=world, device=local_rank, unique_id=bytes(uid.cpu().numpy().tobytes()))
+        driver.upload_keys(keys.data_ptr() if rank == 0 else None, L,
+                           scales=key_scales.data_ptr() if (fp8 and rank == 0) else None, root=0)
+        ix = capi.Indexer.borrow(driver.ctx(0), cfg)
+        # the rank's rows run in slices; the NCCL gather of slice i (second stream) runs under the kernels of slice i+1:
+        # at 8 GPUs the gather of the indices costs about half of the per-rank compute
+        n_slices = a.slices or (4 if nq > 8192 else 2)
+    else:
+        ix = capi.Indexer(cfg, local_rank)
+        ix.upload_keys(keys.data_ptr(), seq_len=L, scales=key_scales.data_ptr() if fp8 else None)
     ix.pool_build()
     ix.synchronize()
     stream = torch.cuda.ExternalStream(capi.lib().hisa_cuda_stream(ix._ctx), device=dev)
@@ -287,22 +473,11 @@ def run_b200(a, rank, world, local_rank):
     pool_ms = pe0.elapsed_time(pe1) / pool_reps
 
     def step_hisa():
-        if not dist:
+        if driver is None:
             ix.hisa_select_raw(q.data_ptr(), w.data_ptr(), pos.data_ptr(), nq, out_idx.data_ptr(), out_count.data_ptr(),
                                None, None, out_cand.data_ptr())
-            return
-        for i in range(n_slices):
-            r0, r1 = bounds[i], bounds[i + 1]
-            if r1 <= r0:
-                continue
-            ix.hisa_select_raw(q[r0:r1].data_ptr(), w[r0:r1].data_ptr(), pos[r0:r1].data_ptr(), r1 - r0,
-                               out_idx[r0:r1].data_ptr(), out_count[r0:r1].data_ptr(), None, None,
-                               out_cand[r0:r1].data_ptr())
-            slice_done[i].record(stream)
-            with torch.cuda.stream(comm_stream):
-                comm_stream.wait_event(slice_done[i])
-                dist.all_gather_into_tensor(gathered[i], out_idx[r0:r1])
-        stream.wait_stream(comm_stream)  # the step ends when every rank holds every index row
+        else:  # sharded step: select this rank's rows, every rank ends up with all Q index rows
+            driver.select(capi.DIST_HISA, [q.data_ptr()], [w.data_ptr()], [pos.data_ptr()], Q, num_slices=n_slices)
 
     def step_flat():
         ix.dsa_select_raw(q.data_ptr(), w.data_ptr(), pos.data_ptr(), nq, out_idx.data_ptr(), out_count.data_ptr(), None)
@@ -311,6 +486,8 @@ def run_b200(a, rank, world, local_rank):
         for _ in range(warmup):
             fn()
         ix.synchronize()
+        if driver is not None:
+            driver.synchronize()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -326,8 +503,10 @@ def run_b200(a, rank, world, local_rank):
         for _ in range(steps):
             fn()
         with torch.cuda.stream(stream):
-            e1.record()
+            e1.record()  # the driver makes the context's stream wait for the gather: e1 = "this GPU holds every row"
         ix.synchronize()
+        if driver is not None:
+            driver.synchronize()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         stages = ix.stage_times() if profile else None
@@ -346,7 +525,21 @@ def run_b200(a, rank, world, local_rank):
         ms_total, stages, launches = timed(step_hisa, a.steps, a.warmup, profile=True)
     ms_step = ms_total / a.steps
     value = Q * a.steps / (ms_total * 1e-3)
-    hisa_idx = out_idx.clone()  # the device-path result: the host-buffer (e2e) path must reproduce it bit for bit
+    if driver is not None:
+        # this rank's own rows out of its copy of the gathered matrix (+ the candidate sizes, which the sharded step
+        # does not exchange: one plain call for them)
+        ridx, _ = driver.result_ptrs(0)
+        full = torch.empty((Q, k), device=dev, dtype=torch.int32)
+        ix.memcpy(full.data_ptr(), ridx, Q * k * 4)
+        hisa_idx = full[torch.from_numpy(rows.astype(np.int64)).to(dev)].clone()
+        del full
+        ix.hisa_select_raw(q.data_ptr(), w.data_ptr(), pos.data_ptr(), nq, out_idx.data_ptr(), out_count.data_ptr(),
+                           None, None, out_cand.data_ptr())
+        ix.synchronize()
+        sharded_equals_plain = bool(torch.equal(hisa_idx, out_idx))
+    else:
+        sharded_equals_plain = None
+        hisa_idx = out_idx.clone()  # the device-path result: the host-buffer (e2e) path must reproduce it bit for bit
 
     # ---- roofline of the dominant kernel (stage-2 fused scorer): algorithmic flops / live CUDA-event time
     cand_sum = int(out_cand.to(torch.int64).sum().item())
@@ -509,13 +702,57 @@ def run_b200(a, rank, world, local_rank):
                "sample": f"{nrows} uniformly sampled query rows of the timed workload, all host threads, "
                          f"pool build excluded; recall of the GPU result on these rows = {recall:.5f}"}
 
+    q_gib = q.numel() * q.element_size() / 2**30
+    # ---- N > 1: the sharded configuration of BASELINE.json (C4: L = Q = 131072) on the same ranks, a few steps
+    c4 = None
+    if driver is not None and world > 1 and a.seq_len != 131072:
+        try:
+            L4 = 131072
+            rows4 = capi.dist_plan(L4, world, rank)
+            n4 = len(rows4)
+            g.manual_seed(a.seed + 77)
+            k4 = torch.randn((L4, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16) if rank == 0 else None
+            del q
+            torch.cuda.empty_cache()
+            q4 = torch.randn((n4, H, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+            w4 = torch.rand((n4, H), generator=g, device=dev, dtype=torch.float32) + 0.5
+            p4 = torch.from_numpy(rows4.astype(np.int64)).to(dev).to(torch.int32)
+            cfg4 = capi.make_config(B, m, k, H, d, capi.DTYPE_BF16)
+            uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+            if rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(capi.dist_unique_id()), dtype=torch.uint8))
+            dist.broadcast(uid, src=0)
+            with capi.Dist(cfg4, rank=rank, world=world, device=local_rank, unique_id=bytes(uid.cpu().numpy().tobytes())) as d4:
+                d4.upload_keys(k4.data_ptr() if rank == 0 else None, L4, root=0)
+                times = []
+                for it in range(4):
+                    dist.barrier()
+                    d4.select(capi.DIST_HISA, [q4.data_ptr()], [w4.data_ptr()], [p4.data_ptr()], L4, num_slices=4)
+                    t = torch.tensor([d4.last_ms()], device=dev, dtype=torch.float64)  # synchronises
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                    if it:
+                        times.append(float(t.item()))
+            c4 = {"workload": "C4 prefill L=Q=131072 bf16, rows sharded over the ranks, keys NCCL-broadcast, index rows gathered",
+                  "ms_per_step": float(np.median(times)), "queries_per_s": L4 / (float(np.median(times)) * 1e-3), "n_gpus": world}
+        except Exception as exc:
+            c4 = {"error": f"{type(exc).__name__}: {exc}"}
+
+    # ---- the other BASELINE configurations (one GPU each; rank 0 only)
+    configs = None
+    if rank == 0 and world == 1 and not a.no_configs:
+        del out_idx, hisa_idx
+        if "q" in dir():
+            del q
+        torch.cuda.empty_cache()
+        configs = run_configs(a, torch, capi, dev, load_peaks())
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16" if not fp8 else "e4m3 (fp32 accumulate; block scores in bf16 hi|lo)", "data": "synthetic",
             "config": {"workload": workload_name(a),
-                       "l2": f"inputs larger than L2 (q is {q.numel() * q.element_size() / 2**30:.1f} GiB per step)",
+                       "l2": f"inputs larger than L2 (q is {q_gib:.1f} GiB per step)",
                        "sharding": f"query tiles of {TILE_ROWS} rows round-robin over ranks; keys NCCL-broadcast; "
                                    "indices all-gathered inside the step" if world > 1 else "single GPU"},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
@@ -523,9 +760,17 @@ def run_b200(a, rank, world, local_rank):
             "stages_ms_per_step": per_call, "consumer_sparse_attend": consumer,
             "scorer_stall_fraction_of_cta_time": stalls,
             "candidate_pairs_per_step": cand_sum_all,
+            "configs": configs,
+            "multi_gpu": None if driver is None else {
+                "driver": "hisa_cuda_dist_* (C ABI): one rank per process, ncclCommInitRank, keys by ncclBroadcast, rows in "
+                          f"{TILE_ROWS}-row zig-zag tiles, per-tile ncclBroadcast gather on a second stream under the next slice",
+                "slices_per_rank": n_slices, "rows_this_rank": nq, "sharded_result_equals_plain_call": sharded_equals_plain,
+                "c4_128k": c4},
         }
         print(json.dumps(line), flush=True)
     ix.close()
+    if driver is not None:
+        driver.close()
     if dist:
         dist.destroy_process_group()
 
@@ -538,8 +783,21 @@ def main():
     if a.impl == "reference":
         run_reference(a, rank, world)
         return
-    if world != a.gpus and world == 1 and a.gpus > 1:
-        raise SystemExit("bench.py: --gpus N>1 must be launched with torch.distributed.run (one rank per GPU)")
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # plain `python bench.py --gpus N`: launch the N ranks ourselves, exactly as the driver would
+        import socket
+        import subprocess
+        with socket.socket() as sock:
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")          # communicator lines (nranks, NVLS, rings) go to stderr
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.run(cmd, env=env).returncode)
+    if world != a.gpus and not (world == 1 and a.gpus == 1):
+        print(f"bench.py: launched with WORLD_SIZE={world} but --gpus {a.gpus}; using the launcher's world size", file=sys.stderr)
     run_b200(a, rank, world, local_rank)
 
 

@@ -201,13 +201,21 @@ class Indexer:
 
     def __init__(self, cfg: Config, device: int = 0):
         self.cfg = cfg
+        self._owned = True
         self._ctx = C.c_void_p(None)
         _check(lib().hisa_cuda_create(C.c_int(device), C.byref(cfg), C.byref(self._ctx)))
 
+    @classmethod
+    def borrow(cls, ctx, cfg: Config):
+        """Wraps a context somebody else owns (a rank of a Dist driver): same methods, close() leaves it alive."""
+        self = cls.__new__(cls)
+        self.cfg, self._ctx, self._owned = cfg, ctx, False
+        return self
+
     def close(self):
-        if self._ctx:
+        if self._ctx and self._owned:
             lib().hisa_cuda_destroy(self._ctx)
-            self._ctx = C.c_void_p(None)
+        self._ctx = C.c_void_p(None)
 
     def __del__(self):
         try:
@@ -536,6 +544,10 @@ class Dist:
         cnt = np.empty(total_rows, np.uint32)
         _dist_check(lib().hisa_cuda_dist_fetch(self._d, C.c_int(local), _ptr(idx), _ptr(cnt)), self._d)
         return idx, cnt
+
+    def fetch_into(self, idx_addr, count_addr=None, local=0):
+        """like fetch, into caller memory (pinned host addresses make the copy run at link speed)"""
+        _dist_check(lib().hisa_cuda_dist_fetch(self._d, C.c_int(local), _ptr(idx_addr), _ptr(count_addr)), self._d)
 
     def last_ms(self) -> float:
         ms = C.c_float(0.0)
