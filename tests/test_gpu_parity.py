@@ -668,3 +668,194 @@ def test_sharded_rows_equal_unsharded_bit_for_bit(oracle, strategy):
     mcount = np.empty(Q, np.uint32)
     mcount[order[order >= 0]] = counts[order >= 0]
     assert np.array_equal(merged, full["idx"]) and np.array_equal(mcount, full["count"])
+
+
+# ------------------------------------------------------------------------------------------ every BASELINE configuration
+def _stratified_rows(L, B, m, k, n_random, seed):
+    """regime boundaries t + 1 in {k, mB, (m+2)B}, block edges t mod B in {0, B-1}, first / last rows, random rows"""
+    edge = [0, 1, B - 1, B, k - 1, k, k + 1, m * B - 1, m * B, m * B + 1, (m + 2) * B - 1, (m + 2) * B, (m + 2) * B + 1,
+            L // 2 - 1, L // 2, L - B - 1, L - B, L - 2, L - 1]
+    edge = [t for t in edge if 0 <= t < L]
+    rnd = np.random.default_rng(seed).integers(0, L, n_random)
+    return np.unique(np.concatenate([edge, rnd])).astype(np.uint32)
+
+
+def test_config_c1_f32_storage_at_8k(oracle):
+    """BASELINE configs[0] AS SPECIFIED: fp32 q/w/k at L=8K, H=64, d=128, B=128, m=32, k=2048. The f32 storage path
+    (exact 3-way bf16 split, 6 MMA terms) is held to the 1e-5 near-tie rule; hisa and the flat indexer; edge rows + 100
+    random rows against the oracle, regime equivalence on every row of the equivalent prefix."""
+    L, H, d, B, m, k = 8192, 64, 128, 128, 32, 2048
+    pos = np.arange(L, dtype=np.uint32)
+    prob = oracle.make_inputs("random", 1, L, pos, H, d, block_size=B, block_budget=m, token_budget=k)
+    with indexer_for(prob, capi.DTYPE_F32) as ix:
+        ix.upload_keys(prob.keys, check_finite=True)
+        h = ix.hisa_select(prob.queries, prob.gates, pos, check_finite=True)
+        f = ix.dsa_select(prob.queries, prob.gates, pos)
+    rows = _stratified_rows(L, B, m, k, 100, 0)
+    ex_h, near_h, rec_h = compare_selection(oracle, prob, "hisa", h, rows, F32_RTOL)
+    ex_f, near_f, rec_f = compare_selection(oracle, prob, "dsa", f, rows, F32_RTOL)
+    print(f"C1 f32: hisa exact={ex_h} near-tie={near_h} recall={rec_h:.6f}; dsa exact={ex_f} near-tie={near_f} recall={rec_f:.6f}")
+    assert rec_h >= 0.999 and rec_f >= 0.999
+    lim = m * B
+    assert np.array_equal(h["idx"][:lim], f["idx"][:lim]) and np.array_equal(h["count"][:lim], f["count"][:lim])
+
+
+def test_config_c2_32k_sampled_rows(oracle):
+    """BASELINE configs[1]: DeepSeek-V3.2 indexer shape at L=32K, bf16."""
+    L, B, m, k = 32768, 128, 64, 2048
+    rows = _stratified_rows(L, B, m, k, 150, 2)
+    prob, qb, kb = _numpy_problem(oracle, L, rows, 32, B, m, k)
+    with indexer_for(prob) as ix:
+        ix.upload_keys(kb)
+        h = ix.hisa_select(qb, prob.gates, rows)
+        f = ix.dsa_select(qb, prob.gates, rows)
+    sel = np.arange(len(rows))
+    ex, near, rec = compare_selection(oracle, prob, "hisa", h, sel, BF16_RTOL)
+    flat_sel = sel[::6]   # the flat oracle costs H * (t + 1) dots per row
+    _, _, rec_f = compare_selection(oracle, prob, "dsa", f, flat_sel, BF16_RTOL)
+    print(f"C2 32K: hisa exact={ex} near-tie={near} of {len(rows)} recall={rec:.6f}; dsa recall={rec_f:.6f} on {len(flat_sel)} rows")
+    assert rec >= 0.999 and rec_f >= 0.999
+    lim = rows < m * B
+    assert np.array_equal(h["idx"][lim], f["idx"][lim])
+
+
+def test_config_c3_fp8_at_64k_sampled_rows(oracle):
+    """BASELINE configs[2], the fp8 variant at FULL size: e4m3 q/k with per-key scales at L=65536, same stratification as
+    the bf16 headline test."""
+    L, B, m, k = 65536, 128, 64, 2048
+    rows = _stratified_rows(L, B, m, k, 120, 3)
+    rng = np.random.default_rng(33)
+    keys = rng.standard_normal((L, 128), dtype=np.float32)
+    q = rng.standard_normal((len(rows), 64, 128), dtype=np.float32)
+    w = rng.uniform(0.5, 1.5, (len(rows), 64)).astype(np.float32)
+    prob = oracle.Problem(q, w, keys, rows, block_size=B, block_budget=m, token_budget=k)
+    q8, k8, ks = quantize_problem_to_fp8(prob)
+    with indexer_for(prob, capi.DTYPE_FP8) as ix:
+        ix.upload_keys(k8, scales=ks)
+        h = ix.hisa_select(q8, prob.gates, rows)
+        f = ix.dsa_select(q8, prob.gates, rows)
+    sel = np.arange(len(rows))
+    ex, near, rec = compare_selection(oracle, prob, "hisa", h, sel, FP8_RTOL)
+    _, _, rec_f = compare_selection(oracle, prob, "dsa", f, sel[::10], FP8_RTOL)
+    print(f"C3 fp8 64K: hisa exact={ex} near-tie={near} of {len(rows)} recall={rec:.6f}; dsa recall={rec_f:.6f}")
+    assert rec >= 0.999 and rec_f >= 0.999
+    lim = rows < m * B
+    assert np.array_equal(h["idx"][lim], f["idx"][lim])
+
+
+def test_config_c4_128k_sampled_rows(oracle):
+    """BASELINE configs[3] (single-GPU leg): prefill at L=131072, bf16."""
+    L, B, m, k = 131072, 128, 64, 2048
+    rows = _stratified_rows(L, B, m, k, 120, 4)
+    prob, qb, kb = _numpy_problem(oracle, L, rows, 34, B, m, k)
+    with indexer_for(prob) as ix:
+        ix.upload_keys(kb)
+        h = ix.hisa_select(qb, prob.gates, rows)
+        f = ix.dsa_select(qb, prob.gates, rows)
+    sel = np.arange(len(rows))
+    ex, near, rec = compare_selection(oracle, prob, "hisa", h, sel, BF16_RTOL)
+    _, _, rec_f = compare_selection(oracle, prob, "dsa", f, sel[::16], BF16_RTOL)
+    print(f"C4 128K: hisa exact={ex} near-tie={near} of {len(rows)} recall={rec:.6f}; dsa recall={rec_f:.6f}")
+    assert rec >= 0.999 and rec_f >= 0.999
+    valid = h["idx"] >= 0
+    assert ((h["idx"] <= rows[:, None].astype(np.int64)) | ~valid).all() and (h["count"] == np.minimum(k, h["cand"])).all()
+
+
+def test_config_c5_decode_at_1m_with_appended_tokens(oracle):
+    """BASELINE configs[4] at L = 1M: 64 queries at the newest position; the last tokens arrive one at a time through the
+    incremental tail-block update (BlockSummaryCache::append, block_summary.hpp:27-30) before each selection; the
+    summaries stay bit-identical to a batch build over all 1M keys."""
+    L, B, m, k, steps = 1048576, 128, 64, 2048, 3
+    rows = np.full(64, L - 1, np.uint32)
+    prob, qb, kb = _numpy_problem(oracle, L, rows, 78, B, m, k)
+    with indexer_for(prob) as ix:
+        ix.upload_keys(kb[:L - steps])
+        ix.pool_build()
+        for s in range(steps):
+            at = L - steps + s
+            ix.pool_append(kb[at:at + 1])
+            pos = np.full(64, at, np.uint32)
+            h = ix.hisa_select(qb, prob.gates, pos)
+            assert (h["count"] == k).all() and (h["blocks"][np.arange(64), h["nblocks"] - 1] == at // B).all()
+            assert (h["blocks"][:, 0] == 0).all() and (h["cand"] <= (m + 2) * B).all()
+        sums, counts, pooled = ix.pool_read()
+    osums, ocounts, opooled = oracle.pool_build(prob.keys, B)
+    assert counts.tolist() == ocounts.tolist() and np.array_equal(sums, osums) and np.array_equal(pooled, opooled)
+    ex, near, rec = compare_selection(oracle, prob, "hisa", h, np.arange(64), BF16_RTOL)
+    print(f"C5 decode 1M: exact={ex} near-tie={near} recall={rec:.6f}")
+    assert rec >= 0.999
+
+
+def test_ratio_4to1_m128_at_64k(oracle):
+    """Fig. 2 panel b (SPEC.md:462 `--mode ratio --ratio 4`): M : m = 4 : 1 at L = 64K, i.e. m = 128 and
+    up to (m + 2) B = 16640 candidates per query."""
+    L, B, m, k = 65536, 128, 128, 2048
+    rows = _stratified_rows(L, B, m, k, 120, 5)
+    prob, qb, kb = _numpy_problem(oracle, L, rows, 35, B, m, k)
+    with indexer_for(prob) as ix:
+        ix.upload_keys(kb)
+        h = ix.hisa_select(qb, prob.gates, rows)
+        f = ix.dsa_select(qb, prob.gates, rows)
+    sel = np.arange(len(rows))
+    ex, near, rec = compare_selection(oracle, prob, "hisa", h, sel, BF16_RTOL)
+    print(f"4:1 m=128 64K: exact={ex} near-tie={near} of {len(rows)} recall={rec:.6f}")
+    assert rec >= 0.999
+    late = rows >= (m + 2) * B
+    assert (h["cand"][late] <= (m + 2) * B).all() and (h["cand"][late] > (m - 1) * B).all() and (h["nblocks"][late] >= m).all()
+    lim = rows < m * B
+    assert np.array_equal(h["idx"][lim], f["idx"][lim])
+
+
+def test_candidate_union_373_on_the_device(oracle):
+    """SPEC.md:220 known answer, through the device path: blocks {0, 2, 3}, B = 128, t = 500 -> 373 candidate tokens.
+    Keys are crafted so that stage 1 selects exactly those blocks (J = [3, 1, 5, 2], m = 2, forced first + last)."""
+    B, L = 128, 512
+    keys = np.zeros((L, 2), np.float32)
+    for b, v in enumerate([3.0, 1.0, 5.0, 2.0]):
+        keys[b * B:(b + 1) * B, 0] = v
+    q = np.float32([[[1.0, 0.0]]])
+    w = np.float32([[1.0]])
+    pos = np.uint32([500])
+    cfg = capi.make_config(B, 2, 200, 1, 2, capi.DTYPE_F32)
+    with capi.Indexer(cfg) as ix:
+        ix.upload_keys(keys)
+        J, ne = ix.score_blocks(q, w, pos)
+        assert ne[0] == 4 and J[0, :4].tolist() == [3.0, 1.0, 5.0, 2.0]
+        bs = ix.block_sparse_select(q, w, pos)
+        assert bs["blocks"][0, :bs["nblocks"][0]].tolist() == [0, 2, 3]
+        assert bs["count"][0] == 373
+        want = oracle.candidate_union(np.uint32([0, 2, 3]), B, 500, L)
+        assert len(want) == 373 and bs["idx"][0, :373].tolist() == want.tolist() and (bs["idx"][0, 373:] == -1).all()
+        h = ix.hisa_select(q, w, pos)
+        assert h["cand"][0] == 373 and h["count"][0] == 200 and set(h["idx"][0, :200].tolist()) <= set(want.tolist())
+        # within the pool every block-2 token (score 5) beats every block-0 token (3), which beats block 3 (2):
+        # 128 + 72 lowest-index tokens of block 0 (SmallestIndex tie-break)
+        assert h["idx"][0, :200].tolist() == list(range(72)) + list(range(256, 384))
+
+
+@pytest.mark.parametrize("pool_tokens", [300, 1000, 1664])
+def test_cache_snapshot_shorter_than_the_inputs(oracle, pool_tokens):
+    """hisa/hisa.hpp:16-21 + block_summary.hpp:27-30: the summaries a caller holds may cover fewer tokens than the key
+    sequence (decode: append, then select). Eligible blocks are clipped to the snapshot's blocks, the forced local block
+    is the last eligible one, candidates still come from the full key sequence. hisa_cuda_pool_set installs the
+    snapshot; the oracle is given the same one."""
+    L, H, d, B, m, k = 2048, 64, 128, 128, 3, 200
+    pos = np.unique(np.concatenate([np.arange(0, L, 37), [pool_tokens - 1, pool_tokens, min(L - 1, pool_tokens + B), L - 1]])).astype(np.uint32)
+    prob = oracle.make_inputs("random", 9, L, pos, H, d, block_size=B, block_budget=m, token_budget=k)
+    qb, kb = round_problem_to_bf16(prob)
+    prob.pool_tokens = pool_tokens
+    osums, ocounts, _ = oracle.pool_build(prob.keys[:pool_tokens], B)
+    with indexer_for(prob) as ix:
+        ix.upload_keys(kb)
+        ix.pool_set(osums, ocounts, pool_tokens)
+        h = ix.hisa_select(qb, prob.gates, pos)
+        b = ix.block_sparse_select(qb, prob.gates, pos)
+        sums, counts, _ = ix.pool_read(num_blocks=len(ocounts))
+    assert np.array_equal(sums, osums) and counts.tolist() == ocounts.tolist()
+    nb = len(ocounts)
+    assert (h["blocks"][np.arange(len(pos)), h["nblocks"] - 1] == np.minimum(pos // B, nb - 1)).all()
+    rows = np.arange(len(pos))
+    ex, near, rec = compare_selection(oracle, prob, "hisa", h, rows, BF16_RTOL)
+    compare_selection(oracle, prob, "block", b, rows, BF16_RTOL)
+    print(f"snapshot of {pool_tokens} tokens: exact={ex} near-tie={near} recall={rec:.6f}")
+    assert rec >= 0.999 and ex + near == len(pos)
