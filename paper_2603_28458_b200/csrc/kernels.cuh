@@ -161,6 +161,7 @@ int launch_score_simt(const ScoreArgs& args, const __nv_bfloat16* a_op, const __
 
 int launch_select(const SelectArgs& args, uint32_t rows, uint32_t n_cap, cudaStream_t stream);
 
+
 // dense work list: chunk-major list of (tile, chunk) items for rows [0, nq) in chunks of `chunk` queries;
 // tile needed iff tile*128 <= min(max position in chunk, seq_len-1) / unit_div.
 int launch_build_dense_work(const uint32_t* pos, uint32_t nq, uint32_t chunk, uint32_t seq_len, uint32_t unit_div,

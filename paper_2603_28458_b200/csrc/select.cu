@@ -805,13 +805,31 @@ __device__ __forceinline__ uint32_t atom_shared_inc(uint32_t addr) {
   return old;
 }
 
+// k[e] for a run-time e: a switch over the (compile-time sized) register array; a few cycles, no memory access
+template <int KPT>
+__device__ __forceinline__ uint32_t pick_key(const uint32_t (&k)[KPT], uint32_t e) {
+  uint32_t v = 0;
+#define HISA_PICK4(b) \
+  case (b): v = k[(b) < KPT ? (b) : 0]; break; case (b) + 1: v = k[(b) + 1 < KPT ? (b) + 1 : 0]; break; \
+  case (b) + 2: v = k[(b) + 2 < KPT ? (b) + 2 : 0]; break; case (b) + 3: v = k[(b) + 3 < KPT ? (b) + 3 : 0]; break;
+  switch (e) {
+    HISA_PICK4(0) HISA_PICK4(4) HISA_PICK4(8) HISA_PICK4(12) HISA_PICK4(16) HISA_PICK4(20) HISA_PICK4(24) HISA_PICK4(28)
+    HISA_PICK4(32) HISA_PICK4(36) HISA_PICK4(40) HISA_PICK4(44) HISA_PICK4(48) HISA_PICK4(52) HISA_PICK4(56) HISA_PICK4(60)
+    default: break;
+  }
+#undef HISA_PICK4
+  return v;
+}
+
 template <int THREADS, int PER4>
-__global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
+// 64 registers per thread: four 256-thread CTAs per SM (at 72 registers three fit, and the kernel is latency-bound per
+// warp: 1.36 -> 1.17 ms at C3 from the fourth CTA alone)
+__global__ void __launch_bounds__(THREADS, THREADS == 256 ? 4 : 2) select_tok_kernel(SelectArgs a) {
   constexpr int KPT = PER4 * 4;
   constexpr uint32_t CAP = THREADS * KPT;
   constexpr int NW = THREADS / 32;
   constexpr int BPT = kBins / THREADS;
-  static_assert(KPT > 32 && KPT <= 64, "two 32-bit emit masks per thread");
+  static_assert(KPT <= 64, "two 32-bit emit masks per thread");
   static_assert(BPT % 4 == 0, "each thread owns whole 16-byte groups of histogram bins");
   extern __shared__ __align__(16) uint32_t smem_u[];
   uint32_t* skey = smem_u;                  // [CAP] scores as delivered by the bulk copy
@@ -903,21 +921,20 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
       k[4 * j + 3] = score_key_fast(v.w);
     }
   }
-  uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
-  if (first + KPT <= n) {
+  // One code path for every thread (a warp that runs a "full" and a "partial" variant side by side arrives late at the
+  // next barrier): non-candidates are key 0, which max() ignores and which k - 1 turns into the largest value for min()
+  if (first + KPT > n) {
 #pragma unroll
-    for (int e = 0; e < KPT; ++e) {
-      kmin = min(kmin, k[e]);
-      kmax = max(kmax, k[e]);
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < KPT; ++e) {
+    for (int e = 0; e < KPT; ++e)
       if (first + e >= n) k[e] = 0u;
-      if (k[e]) kmin = min(kmin, k[e]);
-      kmax = max(kmax, k[e]);
-    }
   }
+  uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+#pragma unroll
+  for (int e = 0; e < KPT; ++e) {
+    kmin = min(kmin, k[e] - 1u);
+    kmax = max(kmax, k[e]);
+  }
+  kmin = first < n ? kmin + 1u : 0xFFFFFFFFu;
   kmin = __reduce_min_sync(0xffffffffu, kmin);
   kmax = __reduce_max_sync(0xffffffffu, kmax);
   if (lane == 0) {
@@ -950,11 +967,12 @@ __global__ void __launch_bounds__(THREADS) select_tok_kernel(SelectArgs a) {
           if (e < 32) or_bit_if_le(h0, k[e] - lo, span, 1u << e);
           else or_bit_if_le(h1, k[e] - lo, span, 1u << (e - 32));
         }
-        if (h0 | h1) {
-#pragma unroll
-          for (int e = 0; e < KPT; ++e)
-            if ((e < 32 ? h0 >> e : h1 >> (e - 32)) & 1u) sts_u32(list_addr + atom_shared_inc(fill_addr) * 4u, k[e]);
-        }
+        // few threads own a key of the threshold range: they fetch it from the register file with a jump over the KPT
+        // cases (pick_key) instead of every warp walking a KPT-way predicated sequence (154 instructions per warp and row)
+        for (uint32_t hh = h0; hh; hh &= hh - 1)
+          sts_u32(list_addr + atom_shared_inc(fill_addr) * 4u, pick_key<KPT>(k, uint32_t(__ffs(hh)) - 1u));
+        for (uint32_t hh = h1; hh; hh &= hh - 1)
+          sts_u32(list_addr + atom_shared_inc(fill_addr) * 4u, pick_key<KPT>(k, 31u + uint32_t(__ffs(hh))));
       }
       __syncthreads();
       if (tid < in_range) {
