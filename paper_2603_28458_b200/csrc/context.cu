@@ -381,7 +381,6 @@ int run_scorer(hisa_cuda_ctx* ctx, const ScoreJob& j) {
   a.a_rows = uint32_t(j.a_rows);
   a.fp8 = j.a8 ? 1u : 0u;
   a.a_scale = j.a_scale;
-  a.debug_flags = env_u32("HISA_TC_DEBUG", 0);
   a.epi_sleep_ns = env_u32("HISA_TC_EPI_SLEEP", 0);
   a.producers = std::min<uint32_t>(std::max<uint32_t>(env_u32("HISA_TC_PRODUCERS", j.a8 ? 2 : 3), 1), 3);
   a.stats = nullptr;

@@ -24,9 +24,12 @@ constexpr int kGroupQ = 4;      // queries per MMA group (UMMA N = 256)
 constexpr int kMaxSeg = 3;
 constexpr int kMaxReplicas = 7;  // peer copies of the selection output (8-GPU box: 7 peers)
 
-// position of head j inside a query's 64-float gate row: heads {4i + c : i = 0..15} are the columns that
-// tcgen05.ld.16x128b hands to the lanes with (lane % 4) == c, and are stored as 16 consecutive floats.
-__host__ __device__ constexpr uint32_t gate_slot(uint32_t j) { return (j % 4) * 16 + j / 4; }
+// position of head j inside a query's 64-float gate row. tcgen05.ld.16x128b hands the columns (heads) {4i + c : i = 0..15}
+// to the lanes with (lane % 4) == c; such a lane reads its 16 gates as four 16-byte pieces h = 0..3 (heads 4(4h + u) + c,
+// u = 0..3). Piece (h, c) lives at float offset h * 16 + c * 4: for one h the four lane classes read 64 CONTIGUOUS bytes,
+// so an LDS.128 of a quarter warp touches every bank once. (Round 1 stored piece (c, h) at c * 16 + h * 4: lane classes
+// 0/2 and 1/3 then hit the same banks — a 2-way conflict on every gate load, 475 M conflict wavefronts per C3 launch.)
+__host__ __device__ constexpr uint32_t gate_slot(uint32_t j) { return ((j / 4) / 4) * 16 + (j % 4) * 4 + (j / 4) % 4; }
 
 // One unit of scorer work: one operand tile against `count` queries.
 //   dense mode: queries are rows first .. first+count-1, results go to out[row, tile*128 + lane]
@@ -56,7 +59,6 @@ struct ScoreArgs {
   const float* a_scale;        // fp8: per-row dequantisation scale of the A operand (may be null = 1)
   uint32_t producers;          // TMA producer warps that take part (1..3)
   uint32_t epi_sleep_ns;       // nanosleep between polls of the epilogue warps' accumulator barrier (0 = spin)
-  uint32_t debug_flags;        // timing experiments only (HISA_TC_DEBUG): 1 skip epilogue math, 2 skip query TMA
   unsigned long long* stats;   // optional [kScoreStats] role-level stall cycles, summed over CTAs (may be null)
 };
 

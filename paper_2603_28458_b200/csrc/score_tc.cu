@@ -325,7 +325,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             const uint32_t wbar = smem_u32(&b_full[stage]);
 #pragma unroll
             for (uint32_t qi = 0; qi < kGroupQ; ++qi)
-              if (qi < nvalid && !(a.debug_flags & 4u))
+              if (qi < nvalid)
                 bulk_load_1d_addr(w_smem + (ws * kGroupQ + qi) * kGateRowBytes, a.gates + uint64_t(qrow[qi]) * kHeads,
                                   kGateRowBytes, wbar);
           }
@@ -339,18 +339,14 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
               __syncwarp();
               if (mine && elect_one()) {
                 const uint32_t fbar = smem_u32(&b_full[stage]);
-                const uint32_t gate_bytes = (ib + kh == 0 && !(a.debug_flags & 4u)) ? nvalid * kGateRowBytes : 0u;
-                if (a.debug_flags & 2u) {
-                  mbar_arrive_expect_tx(&b_full[stage], gate_bytes);
-                } else {
-                  mbar_arrive_expect_tx(&b_full[stage], nvalid * kQBoxBytes + gate_bytes);
-                  const uint32_t dst = b_smem + stage * kBChunkBytes;
+                const uint32_t gate_bytes = (ib + kh == 0) ? nvalid * kGateRowBytes : 0u;
+                mbar_arrive_expect_tx(&b_full[stage], nvalid * kQBoxBytes + gate_bytes);
+                const uint32_t dst = b_smem + stage * kBChunkBytes;
 #pragma unroll
-                  for (uint32_t qi = 0; qi < kGroupQ; ++qi)
-                    if (qi < nvalid)
-                      tma_load_2d_addr(dst + qi * kQBoxBytes, &map_b, fbar, ib * kDim + kh * KBOX,
-                                       int32_t(qrow[qi] * kHeads));
-                }
+                for (uint32_t qi = 0; qi < kGroupQ; ++qi)
+                  if (qi < nvalid)
+                    tma_load_2d_addr(dst + qi * kQBoxBytes, &map_b, fbar, ib * kDim + kh * KBOX,
+                                     int32_t(qrow[qi] * kHeads));
               }
               __syncwarp();
               if (++stage == NST) { stage = 0; sph ^= 1u; }
@@ -453,7 +449,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     const uint32_t set = warp >> 3;        // accumulator / group parity this warp serves
     const uint32_t quarter = warp & 3u;
     const uint32_t qp = ((warp >> 2) & 1u) * 2u;  // first of the two queries this warp reduces
-    const uint32_t w_lane = smem_u32(s_w) + qp * kGateRowBytes + (lane & 3u) * 64u;
+    const uint32_t w_lane = smem_u32(s_w) + qp * kGateRowBytes + (lane & 3u) * 16u;  // gate_slot: piece (h, c) at h*64 + c*16
     const uint32_t t_lane = tmem_base + ((quarter * 32u) << 16) + set * kAccCols + qp * kHeads;
     const uint32_t row = quarter * 32 + (lane >> 2) + 8u * (lane & 3u);
     const bool b0 = lane & 1u, b1 = lane & 2u;
@@ -471,15 +467,15 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       if (FP8 && row_ok && a.a_scale) kscale = __ldg(a.a_scale + lds_u32(maddr + 36) + row);
       __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the spin loop
       tc_fence_after();
-      const bool act0 = qp < nvalid && !(a.debug_flags & 1u);
-      const bool act1 = qp + 1 < nvalid && !(a.debug_flags & 1u);
+      const bool act0 = qp < nvalid;
+      const bool act1 = qp + 1 < nvalid;
       const uint32_t waddr = w_lane + ws * (kGroupQ * kGateRowBytes);
       if (act0) {
         // fragment address: + 32 per column half, + 16 lanes per row half, + 64 columns for the second query
         tmem_ld_16x128b_x8(t_lane, vx);                                // F(0, 0, 0)
         float4 gw[4];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) gw[h] = lds_f4(waddr + h * 16);
+        for (int h = 0; h < 4; ++h) gw[h] = lds_f4(waddr + h * 64);
         const uint2 qrows = lds_u2(maddr + qp * 4), qcols = lds_u2(maddr + 16 + qp * 4);
         float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
         RowSum f;
@@ -499,7 +495,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         float* dst0 = a.out + uint64_t(qrows.x) * a.out_stride + qcols.x + row;
         if (act1) {
 #pragma unroll
-          for (int h = 0; h < 4; ++h) gw[h] = lds_f4(waddr + kGateRowBytes + h * 16);
+          for (int h = 0; h < 4; ++h) gw[h] = lds_f4(waddr + kGateRowBytes + h * 64);
           a0 = a1 = a2 = a3 = make_float2(0.f, 0.f);
           tmem_ld_wait();
           tmem_ld_16x128b_x8(t_lane + kHeads + 32, vy);                // F(1, 0, 1)
