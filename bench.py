@@ -255,14 +255,19 @@ def measure_config(torch, capi, dev, peaks, cid, name, L, rows, B, m, k, dtype="
         stream = torch.cuda.ExternalStream(capi.lib().hisa_cuda_stream(ix._ctx), device=dev)
         state = {"L": L}
 
+        if decode:
+            # every query sits at the newest position: position >= seq_len is the streaming query (inputs.hpp:18-19), so the
+            # position array never changes while keys are appended and the step is two C-ABI calls with constant arguments
+            # (from the third step on hisa_cuda_hisa_select replays one captured CUDA graph)
+            pos.fill_(2 ** 31 - 1)
+            torch.cuda.synchronize()
+
         def step_hisa():
             if decode:
                 at = state["L"]
                 ix.pool_append(keys.data_ptr() + at * d * eb, n=1, key_dim=d,
                                scales=(scales.data_ptr() + at * 4) if scales is not None else None)
                 state["L"] += 1
-                with torch.cuda.stream(stream):
-                    pos.fill_(state["L"] - 1)
             ix.hisa_select_raw(q.data_ptr(), w.data_ptr(), pos.data_ptr(), nq, out_idx.data_ptr(), out_count.data_ptr(),
                                None, None, out_cand.data_ptr())
 

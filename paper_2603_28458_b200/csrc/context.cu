@@ -69,6 +69,23 @@ struct hisa_cuda_ctx {
   DevBuf q_raw, q_op, gates_raw, gates_pad, pos, J, sel, nsel, work, pairs, scalars, cand, flat, out_idx, out_count,
       out_cand, generic_scores, generic_n, export_a, export_b, flag, stats, inv_scratch;
 
+  // decode steps as one graph launch: the device word `dlen` always holds seq_len; a small hisa_select whose arguments
+  // repeat (same device pointers, same Q) is captured once with every kernel reading the sequence length from `dlen`,
+  // and replayed by later calls while the sequence grows underneath it (hisa_cuda_pool_append updates `dlen`)
+  DevBuf dlen;
+  struct GraphSig {
+    const void *q, *g, *pos, *idx, *cnt, *blk, *nblk, *cand, *key_base, *pool_base;
+    uint64_t Q, key_cap;
+    uint32_t Mb;
+    bool operator==(const GraphSig& o) const { return memcmp(this, &o, sizeof *this) == 0; }
+  };
+  GraphSig g_sig{}, g_pending{};
+  cudaGraphExec_t g_exec = nullptr;
+  uint32_t g_seen = 0, g_launches = 0;
+  bool g_enabled = true;
+  bool dyn = false;      // kernels of the current call read the sequence length from dlen
+  uint32_t dyn_Mb = 0;   // upper bound of the number of summarised blocks while the captured graph stays valid
+
   // output placement for row-sharded multi-GPU runs (hisa_cuda_set_output_placement)
   const uint32_t* place_rows = nullptr;
   uint64_t place_q0 = 0;  // first row of the current host-pipeline slice inside the call (select_pipelined)
@@ -343,6 +360,7 @@ int prepare_inputs(hisa_cuda_ctx* ctx, const void* queries, const float* gates, 
 // ------------------------------------------------------------------------------------------------
 struct ScoreJob {
   int stats_slot;  // 0: stage 1, 1: stage 2 / flat
+  uint32_t counter_slot = 0;  // which pair of device scalars holds the work count / cursor (0: sc[0..1], 2: sc[2..3])
   const __nv_bfloat16* a_op;
   uint64_t a_rows;
   uint32_t nseg_a;
@@ -365,8 +383,8 @@ int run_scorer(hisa_cuda_ctx* ctx, const ScoreJob& j) {
   ScoreArgs a{};
   uint32_t* sc = ctx->scalars.as<uint32_t>();
   a.work = ctx->work.as<WorkItem>();
-  a.work_count = sc;
-  a.work_cursor = sc + 1;
+  a.work_count = sc + j.counter_slot;
+  a.work_cursor = sc + j.counter_slot + 1;
   a.pairs = j.pairs;
   a.gates = j.gates;
   a.out = j.out;
@@ -412,7 +430,8 @@ int run_scorer(hisa_cuda_ctx* ctx, const ScoreJob& j) {
 
 // operands of a token-scoring job (stage 2, flat, score_tokens) for query rows [q0, ...)
 void set_token_operands(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, ScoreJob& j) {
-  j.a_rows = ctx->seq_len;
+  // graph replay: the map covers the whole key allocation, rows beyond the live sequence are never selected
+  j.a_rows = ctx->dyn ? ctx->key_cap : ctx->seq_len;
   j.terms = ctx->terms_tok;
   if (ctx->fp8) {
     j.a8 = ctx->key_op.as<uint8_t>();
@@ -424,6 +443,25 @@ void set_token_operands(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, Scor
     j.nseg_a = ctx->nseg_k;
     j.q_op = p.q_op + q0 * kHeads * ctx->nseg_q * kDim;
   }
+}
+
+void drop_graph(hisa_cuda_ctx* ctx) {
+  if (ctx->g_exec) cudaGraphExecDestroy(ctx->g_exec);
+  ctx->g_exec = nullptr;
+  ctx->g_seen = 0;
+  memset(&ctx->g_sig, 0, sizeof ctx->g_sig);
+  memset(&ctx->g_pending, 0, sizeof ctx->g_pending);
+}
+
+// Upper bound of the block count under which a captured decode graph stays valid: the next boundary at which
+// launch_select would pick another kernel variant for the block scores, clipped to the rows the pooled operand has.
+uint32_t block_bucket(const hisa_cuda_ctx* ctx, uint32_t M) {
+  static const uint32_t bounds[] = {128u, 512u, 1024u, 9216u, 18432u, 36864u, 49152u};
+  uint32_t b = 0xFFFFFFFFu;
+  for (uint32_t x : bounds)
+    if (M <= x) { b = x; break; }
+  const uint64_t alloc = ctx->key_cap / ctx->cfg.block_size + 1;  // rows of pooled_op (grow_keys)
+  return uint32_t(std::min<uint64_t>(b, alloc));
 }
 
 int ensure_pool(hisa_cuda_ctx* ctx) {
@@ -455,7 +493,7 @@ uint32_t list_chunk_for(const hisa_cuda_ctx* ctx, uint64_t nq) {
 
 // stage 1: J[q, b] for rows [0, nq) -> ctx->J with stride Mpad
 int run_score_blocks(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, uint64_t nq, uint32_t Mpad) {
-  const uint32_t M = uint32_t(pool_blocks_of(ctx));
+  const uint32_t M = ctx->dyn ? ctx->dyn_Mb : uint32_t(pool_blocks_of(ctx));
   const uint32_t ntiles = Mpad / kTileRows;
   const uint32_t chunk = dense_chunk_for(ctx, nq, ntiles);
   const uint32_t nchunks = uint32_t((nq + chunk - 1) / chunk);
@@ -463,9 +501,10 @@ int run_score_blocks(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, uint64_
   HISA_TRY(ensure(ctx, ctx->J, size_t(nq) * Mpad * sizeof(float)));
   uint32_t* sc = ctx->scalars.as<uint32_t>();
   StageTimer timer(ctx, kStScoreBlocks);
+  // sc[2], sc[3]: the counters of the stage-2 work list, cleared by this kernel (one launch less per call)
   count_launches(ctx, launch_build_dense_work(p.pos + q0, uint32_t(nq), chunk, uint32_t(ctx->seq_len),
                                               ctx->cfg.block_size, ntiles, ctx->work.as<WorkItem>(), sc, sc + 1,
-                                              ctx->stream));
+                                              ctx->dyn ? ctx->dlen.as<uint32_t>() : nullptr, sc + 2, sc + 3, ctx->stream));
   ScoreJob j{};
   j.a_op = ctx->pooled_op.as<__nv_bfloat16>();
   j.a_rows = M;
@@ -490,7 +529,8 @@ int run_select_blocks(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, uint64
   s.stride = Mpad;
   s.pos = p.pos + q0;
   s.seq_len = uint32_t(ctx->seq_len);
-  s.num_blocks = uint32_t(pool_blocks_of(ctx));
+  s.num_blocks = ctx->dyn ? ctx->dyn_Mb : uint32_t(pool_blocks_of(ctx));
+  s.dyn_len = ctx->dyn ? ctx->dlen.as<uint32_t>() : nullptr;
   s.block_size = ctx->cfg.block_size;
   s.keep = ctx->cfg.block_budget;
   s.mode = kSelBlocks;
@@ -547,7 +587,7 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
   const hisa_cuda_config& c = ctx->cfg;
   const uint32_t B = c.block_size, S = c.block_budget + 2, k = c.token_budget;
   const uint32_t L = uint32_t(ctx->seq_len);
-  const uint32_t M = uint32_t(strat == kDsa ? num_blocks_of(ctx) : pool_blocks_of(ctx));
+  const uint32_t M = ctx->dyn ? ctx->dyn_Mb : uint32_t(strat == kDsa ? num_blocks_of(ctx) : pool_blocks_of(ctx));
   const uint32_t Mpad = round_up(M, kTileRows);
   const uint32_t Lpad = round_up(L, kTileRows);
   const uint32_t out_width = strat == kBlockSparse ? S * B : k;
@@ -611,7 +651,7 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
       {
         StageTimer timer(ctx, kStScoreTokens);
         count_launches(ctx, launch_build_dense_work(p.pos + q0, uint32_t(nq), chunk, L, 1, ntiles,
-                                                    ctx->work.as<WorkItem>(), sc, sc + 1, ctx->stream));
+                                                    ctx->work.as<WorkItem>(), sc, sc + 1, nullptr, nullptr, nullptr, ctx->stream));
         ScoreJob j{};
         j.stats_slot = 1;
         set_token_operands(ctx, p, q0, j);
@@ -680,8 +720,9 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
         {
           StageTimer timer(ctx, kStInvert);
           const int n_inv = launch_invert_selection(sel, nsel, S, uint32_t(nq), chunk_list, M, B, spb, split,
-                                                    ctx->work.as<WorkItem>(), sc, sc + 1, ctx->pairs.as<uint2>(),
-                                                    inv_words ? ctx->inv_scratch.as<uint32_t>() : nullptr, ctx->stream);
+                                                    ctx->work.as<WorkItem>(), sc + 2, sc + 3, ctx->pairs.as<uint2>(),
+                                                    inv_words ? ctx->inv_scratch.as<uint32_t>() : nullptr,
+                                                    /*counters_zeroed=*/true, ctx->stream);
           if (n_inv < 0)
             return fail(ctx, HISA_ERR_UNSUPPORTED, "invert selection: %u key blocks need more shared memory than an SM has", M);
           count_launches(ctx, n_inv);
@@ -697,6 +738,7 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
           j.out = ctx->cand.as<float>();
           j.out_stride = cand_cols;
           j.list_mode = true;
+          j.counter_slot = 2;
           j.pairs = ctx->pairs.as<uint2>();
           j.max_items = uint32_t(std::min<uint64_t>(items_cap, 0xFFFFFFFFull));
           ctx->items2 += j.max_items;
@@ -716,6 +758,7 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
           s.sel = sel;
           s.nsel = nsel;
           s.sel_stride = S;
+          s.dyn_len = ctx->dyn ? ctx->dlen.as<uint32_t>() : nullptr;
           s.tie_break = c.tie_break;
           s.out_idx = idx_dst;
           s.out_stride = out_width;
@@ -723,7 +766,8 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
           s.out_count = cnt_dst;
           s.out_cand = cand_dst;
           place(s, q0);
-          count_launches(ctx, launch_select(s, uint32_t(nq), uint32_t(std::min<uint64_t>(cand_cols, L)), ctx->stream));
+          // (graph replay: the variant must not depend on the current length)
+          count_launches(ctx, launch_select(s, uint32_t(nq), uint32_t(ctx->dyn ? cand_cols : std::min<uint64_t>(cand_cols, L)), ctx->stream));
           HISA_TRY(check_launch(ctx, "top-k"));
         }
       }
@@ -868,6 +912,81 @@ int select_pipelined(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, co
   return HISA_OK;
 }
 
+// Small hisa_select calls whose arguments repeat (a decode loop: same device buffers, same Q, the sequence one key
+// longer each time) become ONE graph launch. Call 1 of a signature runs normally; call 2 runs with every kernel reading
+// the sequence length from ctx->dlen and with operand maps / strides sized for the block-count bucket (this sizes all
+// buffers); call 3 captures that same launch sequence into a graph; later calls replay it. Nothing is ever computed
+// differently: the graph holds the same kernels with the same arguments.
+constexpr uint64_t kGraphMaxRows = 2048;
+
+int select_maybe_graph(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const float* gates, const uint32_t* positions,
+                       uint64_t Q, int check_finite, int32_t* out_idx, uint32_t* out_count, int32_t* out_blocks,
+                       uint32_t* out_nblocks, uint32_t* out_cand) {
+  const bool eligible = ctx->g_enabled && strat == kHisa && Q > 0 && Q <= kGraphMaxRows && !check_finite && !ctx->profiling &&
+                        !ctx->pool_external && !ctx->place_rows && !ctx->place_nrep && ctx->pooled_tokens == ctx->seq_len &&
+                        ctx->dlen.p != nullptr;
+  if (!eligible)
+    return select_core(ctx, strat, queries, gates, positions, Q, check_finite, out_idx, out_count, out_blocks, out_nblocks, out_cand);
+  hisa_cuda_ctx::GraphSig sig;
+  memset(&sig, 0, sizeof sig);
+  sig.q = queries; sig.g = gates; sig.pos = positions; sig.idx = out_idx; sig.cnt = out_count; sig.blk = out_blocks;
+  sig.nblk = out_nblocks; sig.cand = out_cand; sig.key_base = ctx->key_op.p; sig.pool_base = ctx->pooled_op.p;
+  sig.Q = Q; sig.key_cap = ctx->key_cap;
+  sig.Mb = block_bucket(ctx, uint32_t(num_blocks_of(ctx)));
+  if (ctx->g_exec && sig == ctx->g_sig) {
+    CU_TRY(ctx, cudaGraphLaunch(ctx->g_exec, ctx->stream));
+    count_launches(ctx, int(ctx->g_launches));
+    return HISA_OK;
+  }
+  if (sig == ctx->g_pending) ++ctx->g_seen;
+  else { ctx->g_pending = sig; ctx->g_seen = 1; }
+  if (ctx->g_seen == 1)
+    return select_core(ctx, strat, queries, gates, positions, Q, check_finite, out_idx, out_count, out_blocks, out_nblocks, out_cand);
+  ctx->dyn = true;
+  ctx->dyn_Mb = sig.Mb;
+  if (ctx->g_seen == 2) {
+    const int rc = select_core(ctx, strat, queries, gates, positions, Q, check_finite, out_idx, out_count, out_blocks, out_nblocks, out_cand);
+    ctx->dyn = false;
+    return rc;
+  }
+  // capture; any failure falls back to plain launches and switches the graph path off for this context
+  const uint64_t before = ctx->call_launches, before_all = ctx->launches;
+  cudaGraph_t graph = nullptr;
+  int rc = HISA_OK;
+  if (cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->g_enabled = false;
+    ctx->dyn = false;
+    return select_core(ctx, strat, queries, gates, positions, Q, check_finite, out_idx, out_count, out_blocks, out_nblocks, out_cand);
+  }
+  rc = select_core(ctx, strat, queries, gates, positions, Q, check_finite, out_idx, out_count, out_blocks, out_nblocks, out_cand);
+  const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+  ctx->dyn = false;
+  const uint32_t captured = uint32_t(ctx->call_launches - before);
+  ctx->call_launches = before;  // nothing ran yet
+  ctx->launches = before_all;
+  if (rc != HISA_OK || ce != cudaSuccess || !graph) {
+    cudaGetLastError();
+    if (graph) cudaGraphDestroy(graph);
+    ctx->g_enabled = false;
+    return select_core(ctx, strat, queries, gates, positions, Q, check_finite, out_idx, out_count, out_blocks, out_nblocks, out_cand);
+  }
+  drop_graph(ctx);
+  const cudaError_t ie = cudaGraphInstantiate(&ctx->g_exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) {
+    cudaGetLastError();
+    ctx->g_exec = nullptr;
+    ctx->g_enabled = false;
+    return select_core(ctx, strat, queries, gates, positions, Q, check_finite, out_idx, out_count, out_blocks, out_nblocks, out_cand);
+  }
+  ctx->g_sig = sig;
+  ctx->g_launches = captured;
+  CU_TRY(ctx, cudaGraphLaunch(ctx->g_exec, ctx->stream));
+  count_launches(ctx, int(captured));
+  return HISA_OK;
+}
+
 int select_impl(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const float* gates, const uint32_t* positions,
                 uint64_t Q, int check_finite, int32_t* out_idx, uint32_t* out_count, int32_t* out_blocks,
                 uint32_t* out_nblocks, uint32_t* out_cand) {
@@ -888,9 +1007,12 @@ int select_impl(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
   if (any_host && ctx->pipe_rows && Q > ctx->pipe_rows)
     rc = select_pipelined(ctx, strat, queries, gates, positions, Q, check_finite, out_idx, out_count, out_blocks,
                           out_nblocks, out_cand);
-  else
+  else if (any_host)
     rc = select_core(ctx, strat, queries, gates, positions, Q, check_finite, out_idx, out_count, out_blocks, out_nblocks,
                      out_cand);
+  else
+    rc = select_maybe_graph(ctx, strat, queries, gates, positions, Q, check_finite, out_idx, out_count, out_blocks,
+                            out_nblocks, out_cand);
   HISA_TRY(rc);
   end_call(ctx);
   return HISA_OK;
@@ -1061,6 +1183,7 @@ int hisa_cuda_create(int device, const hisa_cuda_config* cfg, hisa_cuda_ctx** ou
   ctx->chunk_list = std::max<uint32_t>(env_u32("HISA_CHUNK_LIST", 512), 4);
   ctx->workspace_bytes = uint64_t(std::max<uint32_t>(env_u32("HISA_WORKSPACE_MB", 4096), 16)) << 20;
   ctx->pipe_rows = env_u32("HISA_PIPE_ROWS", 4096);  // 0 disables the host-buffer pipeline
+  ctx->g_enabled = env_u32("HISA_DECODE_GRAPH", 1) != 0;
   *out = ctx;
   return HISA_OK;
 }
@@ -1069,6 +1192,8 @@ int hisa_cuda_destroy(hisa_cuda_ctx* ctx) {
   if (!ctx) return HISA_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  drop_graph(ctx);
+  release(ctx->dlen);
   for (DevBuf* b : {&ctx->key_op, &ctx->key_raw, &ctx->key_scale, &ctx->sums, &ctx->counts, &ctx->pooled_op, &ctx->q_raw, &ctx->q_op,
                     &ctx->gates_raw, &ctx->gates_pad, &ctx->pos, &ctx->J, &ctx->sel, &ctx->nsel, &ctx->work, &ctx->pairs,
                     &ctx->scalars, &ctx->cand, &ctx->flat, &ctx->out_idx, &ctx->out_count, &ctx->out_cand,
@@ -1140,6 +1265,7 @@ int hisa_cuda_memcpy(hisa_cuda_ctx* ctx, void* dst, const void* src, size_t byte
 
 static int grow_keys(hisa_cuda_ctx* ctx, uint64_t need_tokens) {
   if (need_tokens <= ctx->key_cap) return HISA_OK;
+  drop_graph(ctx);  // the captured kernels hold the old operand addresses
   uint64_t cap = std::max<uint64_t>(need_tokens, ctx->key_cap + ctx->key_cap / 2);
   cap = round_up64(cap, 1024);
   const size_t row_bytes = ctx->fp8 ? size_t(kDim) : size_t(ctx->nseg_k) * kDim * sizeof(__nv_bfloat16);
@@ -1210,15 +1336,18 @@ static int ingest_keys(hisa_cuda_ctx* ctx, const void* keys, const float* scales
 }
 
 static int pool_update(hisa_cuda_ctx* ctx, uint64_t first, uint64_t n) {
+  // the kernel also publishes the new sequence length (first + n) in the device word replayed graphs read
+  HISA_TRY(ensure(ctx, ctx->dlen, 16));
   if (ctx->fp8)
     count_launches(ctx, launch_pool_update_fp8(ctx->key_op.as<uint8_t>(), ctx->key_scale.as<float>(), first, n,
                                                ctx->cfg.block_size, ctx->cfg.pool_mode, ctx->sums.as<double>(),
                                                ctx->counts.as<uint32_t>(), ctx->pooled_op.as<__nv_bfloat16>(), ctx->nseg_p,
-                                               ctx->stream));
+                                               ctx->dlen.as<uint32_t>(), ctx->stream));
   else
     count_launches(ctx, launch_pool_update(ctx->key_op.as<__nv_bfloat16>(), ctx->nseg_k, first, n, ctx->cfg.block_size,
                                            ctx->cfg.dim, ctx->cfg.pool_mode, ctx->sums.as<double>(), ctx->counts.as<uint32_t>(),
-                                           ctx->pooled_op.as<__nv_bfloat16>(), ctx->nseg_p, ctx->stream));
+                                           ctx->pooled_op.as<__nv_bfloat16>(), ctx->nseg_p, ctx->dlen.as<uint32_t>(),
+                                           ctx->stream));
   return HISA_OK;
 }
 
@@ -1232,9 +1361,14 @@ static int upload_keys_impl(hisa_cuda_ctx* ctx, const void* keys, const float* s
   ctx->seq_len = 0;
   ctx->pooled_tokens = 0;
   ctx->pool_external = false;
+  drop_graph(ctx);
   HISA_TRY(grow_keys(ctx, seq_len));
   HISA_TRY(ingest_keys(ctx, keys, scales, 0, seq_len, check_finite));
   ctx->seq_len = seq_len;
+  HISA_TRY(ensure(ctx, ctx->dlen, 16));
+  const uint32_t len32 = uint32_t(seq_len);
+  CU_TRY(ctx, cudaMemcpyAsync(ctx->dlen.p, &len32, sizeof len32, cudaMemcpyHostToDevice, ctx->stream));
+  CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // len32 lives on this stack frame
   return HISA_OK;
 }
 
@@ -1307,6 +1441,7 @@ int hisa_cuda_pool_set(hisa_cuda_ctx* ctx, const double* sums, const uint32_t* c
   HISA_TRY(check_launch(ctx, "pool import"));
   CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // the caller's host arrays may go away after the call
   ctx->pool_external = true;
+  drop_graph(ctx);
   ctx->pool_blocks = M;
   ctx->pooled_tokens = std::min<uint64_t>(num_tokens, ctx->seq_len);
   return HISA_OK;
@@ -1508,7 +1643,7 @@ int hisa_cuda_score_tokens(hisa_cuda_ctx* ctx, const void* queries, const float*
   uint32_t* sc = ctx->scalars.as<uint32_t>();
   StageTimer* timer = new StageTimer(ctx, kStScoreTokens);
   count_launches(ctx, launch_build_dense_work(p.pos, uint32_t(Q), chunk, L, 1, ntiles, ctx->work.as<WorkItem>(),
-                                              sc, sc + 1, ctx->stream));
+                                              sc, sc + 1, nullptr, nullptr, nullptr, ctx->stream));
   ScoreJob j{};
   set_token_operands(ctx, p, 0, j);
   j.nq = Q;

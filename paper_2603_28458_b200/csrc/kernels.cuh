@@ -102,6 +102,7 @@ struct SelectArgs {
   const uint32_t* pos;   // [rows] query positions (modes 0,1,2)
   const uint32_t* n_in;  // [rows] candidate counts (modes 3,4)
   uint32_t seq_len, num_blocks, block_size, keep;  // keep = k (tokens) or m (blocks)
+  const uint32_t* dyn_len;  // non-null: seq_len (and num_blocks = ceil(seq_len / block_size)) are read from this device word
   uint32_t mode;
   const int32_t* sel;  // mode 2: [rows, sel_stride] selected blocks ascending
   const uint32_t* nsel;
@@ -166,15 +167,17 @@ int launch_select(const SelectArgs& args, uint32_t rows, uint32_t n_cap, cudaStr
 
 // dense work list: chunk-major list of (tile, chunk) items for rows [0, nq) in chunks of `chunk` queries;
 // tile needed iff tile*128 <= min(max position in chunk, seq_len-1) / unit_div.
+// dyn_len (may be null): device word holding the sequence length (graph replay); zero_a / zero_b (may be null): two more
+// device counters the kernel clears (the stage-2 work list's, saving that list builder a launch)
 int launch_build_dense_work(const uint32_t* pos, uint32_t nq, uint32_t chunk, uint32_t seq_len, uint32_t unit_div,
                             uint32_t ntiles, WorkItem* work, uint32_t* work_count, uint32_t* work_cursor,
-                            cudaStream_t stream);
+                            const uint32_t* dyn_len, uint32_t* zero_a, uint32_t* zero_b, cudaStream_t stream);
 // list work: per chunk of queries, the per-block lists of (row, slot*B) pairs and one item per (block, seg)
 // `split`: most queries one work item may carry (0 = unlimited); longer per-block lists become several items
 int launch_invert_selection(const int32_t* sel, const uint32_t* nsel, uint32_t sel_stride, uint32_t nq,
                             uint32_t chunk, uint32_t num_blocks, uint32_t block_size, uint32_t segs_per_block,
                             uint32_t split, WorkItem* work, uint32_t* work_count, uint32_t* work_cursor, uint2* pairs,
-                            uint32_t* global_counters, cudaStream_t stream);
+                            uint32_t* global_counters, bool counters_zeroed, cudaStream_t stream);
 // words of global scratch launch_invert_selection needs for its per-block counters (0: they fit in shared memory)
 size_t invert_global_words(uint32_t nq, uint32_t chunk, uint32_t num_blocks);
 size_t invert_smem_limit();
@@ -192,12 +195,13 @@ int launch_permute_gates(const float* src, uint64_t rows, uint32_t heads, float*
 int launch_check_finite(const void* src, uint32_t src_type, uint64_t n, uint32_t* flag, cudaStream_t stream);
 int launch_check_positions(const uint32_t* pos, uint64_t n, uint32_t seq_len, uint32_t* flag, cudaStream_t stream);
 // block summaries over tokens [first, first+n): double sums, counts, pooled operand (nseg_p segments)
+// len_out (may be null): device word that receives first + n, the sequence length after the update
 int launch_pool_update(const __nv_bfloat16* key_op, uint32_t nseg_k, uint64_t first, uint64_t n, uint32_t block_size,
                        uint32_t dim, uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op,
-                       uint32_t nseg_p, cudaStream_t stream);
+                       uint32_t nseg_p, uint32_t* len_out, cudaStream_t stream);
 int launch_pool_update_fp8(const uint8_t* key8, const float* key_scale, uint64_t first, uint64_t n, uint32_t block_size,
                            uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op, uint32_t nseg_p,
-                           cudaStream_t stream);
+                           uint32_t* len_out, cudaStream_t stream);
 // installs caller-provided summaries: src_sums f64 [num_blocks, dim], src_counts [num_blocks] (device pointers)
 int launch_pool_import(const double* src_sums, const uint32_t* src_counts, uint32_t num_blocks, uint32_t dim,
                        uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op, uint32_t nseg_p,

@@ -128,9 +128,11 @@ __global__ void check_positions_kernel(const uint32_t* __restrict__ pos, uint64_
 __global__ void __launch_bounds__(kDim)
 pool_update_kernel(const __nv_bfloat16* __restrict__ key_op, uint32_t nseg_k, uint64_t first, uint64_t n,
                    uint32_t block_size, uint32_t pool_max, double* __restrict__ sums,
-                   uint32_t* __restrict__ counts, __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p) {
+                   uint32_t* __restrict__ counts, __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p,
+                   uint32_t* __restrict__ len_out) {
   const uint64_t b = first / block_size + blockIdx.x;
   const uint32_t c = threadIdx.x;
+  if (len_out && blockIdx.x == 0 && c == 0) *len_out = uint32_t(first + n);
   const uint64_t blk_lo = b * block_size;
   const uint64_t s_lo = first > blk_lo ? first : blk_lo;
   const uint64_t blk_hi = blk_lo + block_size;
@@ -173,9 +175,11 @@ pool_update_kernel(const __nv_bfloat16* __restrict__ key_op, uint32_t nseg_k, ui
 __global__ void __launch_bounds__(kDim)
 pool_update_fp8_kernel(const uint8_t* __restrict__ key8, const float* __restrict__ key_scale, uint64_t first, uint64_t n,
                        uint32_t block_size, uint32_t pool_max, double* __restrict__ sums,
-                       uint32_t* __restrict__ counts, __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p) {
+                       uint32_t* __restrict__ counts, __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p,
+                       uint32_t* __restrict__ len_out) {
   const uint64_t b = first / block_size + blockIdx.x;
   const uint32_t c = threadIdx.x;
+  if (len_out && blockIdx.x == 0 && c == 0) *len_out = uint32_t(first + n);
   const uint64_t blk_lo = b * block_size;
   const uint64_t s_lo = first > blk_lo ? first : blk_lo;
   const uint64_t blk_hi = blk_lo + block_size;
@@ -218,8 +222,10 @@ template <bool FP8>
 __global__ void __launch_bounds__(kDim)
 pool_update_staged_kernel(const void* __restrict__ key_op, const float* __restrict__ key_scale, uint32_t nseg_k,
                           uint64_t first, uint64_t n, uint32_t block_size, uint32_t pool_max, double* __restrict__ sums,
-                          uint32_t* __restrict__ counts, __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p) {
+                          uint32_t* __restrict__ counts, __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p,
+                          uint32_t* __restrict__ len_out) {
   extern __shared__ __align__(128) unsigned char pool_smem[];
+  if (len_out && blockIdx.x == 0 && threadIdx.x == 0) *len_out = uint32_t(first + n);
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ float s_scale[2][kPoolChunkRows];
   const uint64_t b = first / block_size + blockIdx.x;
@@ -308,7 +314,7 @@ pool_update_staged_kernel(const void* __restrict__ key_op, const float* __restri
 template <bool FP8>
 bool launch_pool_staged(const void* key_op, const float* key_scale, uint32_t nseg_k, uint64_t first, uint64_t n,
                         uint32_t block_size, uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op,
-                        uint32_t nseg_p, cudaStream_t stream) {
+                        uint32_t nseg_p, uint32_t* len_out, cudaStream_t stream) {
   // decode-sized appends stay on the direct kernel: nothing to stage for a handful of rows
   if (n < 32 || reinterpret_cast<uintptr_t>(key_op) % 16 != 0) return false;
   const uint32_t row_bytes = FP8 ? uint32_t(kDim) : nseg_k * uint32_t(kDim) * 2u;
@@ -317,7 +323,7 @@ bool launch_pool_staged(const void* key_op, const float* key_scale, uint32_t nse
   if (smem > 48 * 1024 && !smem_opt_in(reinterpret_cast<const void*>(kern), smem)) return false;
   const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
   kern<<<uint32_t(b1 - b0 + 1), kDim, smem, stream>>>(key_op, key_scale, nseg_k, first, n, block_size, pool_max, sums, counts,
-                                                      pooled_op, nseg_p);
+                                                      pooled_op, nseg_p, len_out);
   return true;
 }
 
@@ -396,25 +402,25 @@ int launch_check_positions(const uint32_t* pos, uint64_t n, uint32_t seq_len, ui
 
 int launch_pool_update(const __nv_bfloat16* key_op, uint32_t nseg_k, uint64_t first, uint64_t n, uint32_t block_size,
                        uint32_t /*dim*/, uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op,
-                       uint32_t nseg_p, cudaStream_t stream) {
+                       uint32_t nseg_p, uint32_t* len_out, cudaStream_t stream) {
   if (n == 0) return 0;
-  if (launch_pool_staged<false>(key_op, nullptr, nseg_k, first, n, block_size, pool_max, sums, counts, pooled_op, nseg_p, stream))
+  if (launch_pool_staged<false>(key_op, nullptr, nseg_k, first, n, block_size, pool_max, sums, counts, pooled_op, nseg_p, len_out, stream))
     return 1;
   const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
   pool_update_kernel<<<uint32_t(b1 - b0 + 1), kDim, 0, stream>>>(key_op, nseg_k, first, n, block_size, pool_max, sums,
-                                                                 counts, pooled_op, nseg_p);
+                                                                 counts, pooled_op, nseg_p, len_out);
   return 1;
 }
 
 int launch_pool_update_fp8(const uint8_t* key8, const float* key_scale, uint64_t first, uint64_t n, uint32_t block_size,
                            uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op, uint32_t nseg_p,
-                           cudaStream_t stream) {
+                           uint32_t* len_out, cudaStream_t stream) {
   if (n == 0) return 0;
-  if (launch_pool_staged<true>(key8, key_scale, 1, first, n, block_size, pool_max, sums, counts, pooled_op, nseg_p, stream))
+  if (launch_pool_staged<true>(key8, key_scale, 1, first, n, block_size, pool_max, sums, counts, pooled_op, nseg_p, len_out, stream))
     return 1;
   const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
   pool_update_fp8_kernel<<<uint32_t(b1 - b0 + 1), kDim, 0, stream>>>(key8, key_scale, first, n, block_size, pool_max, sums,
-                                                                     counts, pooled_op, nseg_p);
+                                                                     counts, pooled_op, nseg_p, len_out);
   return 1;
 }
 

@@ -27,6 +27,13 @@ constexpr int kBins = 2048;
 constexpr int kBinBits = 11;
 constexpr int kListCap = 1024;  // survivors of the first radix level are compacted when they fit here
 
+// Sequence length / number of summarised blocks of a launch: by value, or read from device memory when the launch is
+// part of a replayed CUDA graph (decode: the sequence grows by one key per step while the graph stays the same).
+__device__ __forceinline__ uint32_t seq_len_of(const SelectArgs& a) { return a.dyn_len ? __ldg(a.dyn_len) : a.seq_len; }
+__device__ __forceinline__ uint32_t num_blocks_of(const SelectArgs& a) {
+  return a.dyn_len ? (__ldg(a.dyn_len) + a.block_size - 1) / a.block_size : a.num_blocks;
+}
+
 __device__ __forceinline__ uint32_t score_key(float f) {
   uint32_t b = __float_as_uint(f);
   if (b == 0x80000000u) b = 0u;  // -0 == +0
@@ -102,13 +109,13 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
   uint32_t n = 0;
   const int32_t* sel_row = nullptr;
   if (a.mode == kSelFlat) {
-    const uint32_t t = min(a.pos[row], a.seq_len - 1);
+    const uint32_t t = min(a.pos[row], seq_len_of(a) - 1);
     n = t + 1;
   } else if (a.mode == kSelBlocks) {
-    const uint32_t t = min(a.pos[row], a.seq_len - 1);
-    n = min(t / B, a.num_blocks - 1) + 1;
+    const uint32_t t = min(a.pos[row], seq_len_of(a) - 1);
+    n = min(t / B, num_blocks_of(a) - 1) + 1;
   } else if (a.mode == kSelCand) {
-    const uint32_t t = min(a.pos[row], a.seq_len - 1);
+    const uint32_t t = min(a.pos[row], seq_len_of(a) - 1);
     const uint32_t ns = a.nsel[row];
     sel_row = a.sel + uint64_t(row) * a.sel_row_stride;
     const uint32_t lastb = uint32_t(sel_row[ns - 1]);
@@ -313,11 +320,11 @@ __global__ void __launch_bounds__(kWarpSelThreads) select_warp_kernel(SelectArgs
   uint32_t n = 0;
   const int32_t* sel_row = nullptr;
   if (a.mode == kSelFlat) {
-    n = min(a.pos[row], a.seq_len - 1) + 1;
+    n = min(a.pos[row], seq_len_of(a) - 1) + 1;
   } else if (a.mode == kSelBlocks) {
-    n = min(min(a.pos[row], a.seq_len - 1) / B, a.num_blocks - 1) + 1;
+    n = min(min(a.pos[row], seq_len_of(a) - 1) / B, num_blocks_of(a) - 1) + 1;
   } else if (a.mode == kSelCand) {
-    const uint32_t t = min(a.pos[row], a.seq_len - 1);
+    const uint32_t t = min(a.pos[row], seq_len_of(a) - 1);
     const uint32_t ns = a.nsel[row];
     sel_row = a.sel + uint64_t(row) * a.sel_row_stride;
     const uint32_t lastb = uint32_t(sel_row[ns - 1]);
@@ -492,11 +499,11 @@ __global__ void __launch_bounds__(THREADS) select_cta_kernel(SelectArgs a) {
   const int32_t* sel_row = nullptr;
   uint32_t ns = 0;
   if (a.mode == kSelFlat) {
-    n = min(a.pos[row], a.seq_len - 1) + 1;
+    n = min(a.pos[row], seq_len_of(a) - 1) + 1;
   } else if (a.mode == kSelBlocks) {
-    n = min(min(a.pos[row], a.seq_len - 1) / B, a.num_blocks - 1) + 1;
+    n = min(min(a.pos[row], seq_len_of(a) - 1) / B, num_blocks_of(a) - 1) + 1;
   } else if (a.mode == kSelCand) {
-    const uint32_t t = min(a.pos[row], a.seq_len - 1);
+    const uint32_t t = min(a.pos[row], seq_len_of(a) - 1);
     ns = a.nsel[row];
     sel_row = a.sel + uint64_t(row) * a.sel_row_stride;
     const uint32_t lastb = uint32_t(sel_row[ns - 1]);
@@ -849,9 +856,9 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? 4 : 2) select_tok_ke
   uint32_t n = 0, ns = 0;
   const int32_t* sel_row = nullptr;
   if (a.mode == kSelFlat) {
-    n = min(a.pos[row], a.seq_len - 1) + 1;
+    n = min(a.pos[row], seq_len_of(a) - 1) + 1;
   } else if (cand) {
-    const uint32_t t = min(a.pos[row], a.seq_len - 1);
+    const uint32_t t = min(a.pos[row], seq_len_of(a) - 1);
     ns = a.nsel[row];
     sel_row = a.sel + uint64_t(row) * a.sel_row_stride;
     const uint32_t lastb = uint32_t(sel_row[ns - 1]);
@@ -1169,9 +1176,18 @@ constexpr int kDenseMaxChunks = 4096;
 __global__ void __launch_bounds__(kDenseThreads)
 build_dense_work_kernel(const uint32_t* __restrict__ pos, uint32_t nq, uint32_t chunk, uint32_t seq_len,
                         uint32_t unit_div, uint32_t ntiles, WorkItem* __restrict__ work,
-                        uint32_t* __restrict__ work_count, uint32_t* __restrict__ work_cursor) {
+                        uint32_t* __restrict__ work_count, uint32_t* __restrict__ work_cursor,
+                        const uint32_t* __restrict__ dyn_len, uint32_t* __restrict__ zero_a, uint32_t* __restrict__ zero_b) {
   __shared__ uint32_t offs[kDenseMaxChunks + 1];
   __shared__ uint32_t scratch[64];
+  if (dyn_len) {  // graph replay: the sequence length lives in device memory; tiles of the operand follow from it
+    seq_len = *dyn_len;
+    ntiles = min(ntiles, ((seq_len + unit_div - 1) / unit_div + kTileRows - 1) / kTileRows);
+  }
+  if (threadIdx.x == 0 && zero_a) {  // the counters of the stage-2 work list, cleared here instead of by a launch of their own
+    *zero_a = 0;
+    *zero_b = 0;
+  }
   const uint32_t nchunks = (nq + chunk - 1) / chunk;
   const uint32_t tid = threadIdx.x;
   // tiles needed by each chunk
@@ -1373,19 +1389,23 @@ int launch_select(const SelectArgs& args_in, uint32_t rows, uint32_t n_cap, cuda
 
 int launch_build_dense_work(const uint32_t* pos, uint32_t nq, uint32_t chunk, uint32_t seq_len, uint32_t unit_div,
                             uint32_t ntiles, WorkItem* work, uint32_t* work_count, uint32_t* work_cursor,
-                            cudaStream_t stream) {
+                            const uint32_t* dyn_len, uint32_t* zero_a, uint32_t* zero_b, cudaStream_t stream) {
   if (nq == 0) return 0;
   build_dense_work_kernel<<<1, kDenseThreads, 0, stream>>>(pos, nq, chunk, seq_len, unit_div, ntiles, work, work_count,
-                                                           work_cursor);
+                                                           work_cursor, dyn_len, zero_a, zero_b);
   return 1;
 }
 
 int launch_invert_selection(const int32_t* sel, const uint32_t* nsel, uint32_t sel_stride, uint32_t nq, uint32_t chunk,
                             uint32_t num_blocks, uint32_t block_size, uint32_t segs_per_block, uint32_t split,
                             WorkItem* work, uint32_t* work_count, uint32_t* work_cursor, uint2* pairs,
-                            uint32_t* global_counters, cudaStream_t stream) {
+                            uint32_t* global_counters, bool counters_zeroed, cudaStream_t stream) {
   if (nq == 0) return 0;
-  zero_two_kernel<<<1, 1, 0, stream>>>(work_count, work_cursor);
+  int launched = 1;
+  if (!counters_zeroed) {
+    zero_two_kernel<<<1, 1, 0, stream>>>(work_count, work_cursor);
+    launched = 2;
+  }
   size_t smem = (size_t(num_blocks) * 2 + 64) * sizeof(uint32_t);
   uint32_t* gcount = nullptr;
   if (smem > invert_smem_limit()) {
@@ -1399,7 +1419,7 @@ int launch_invert_selection(const int32_t* sel, const uint32_t* nsel, uint32_t s
   invert_selection_kernel<<<nchunks, kInvThreads, smem, stream>>>(sel, nsel, sel_stride, nq, chunk, num_blocks,
                                                                   block_size, segs_per_block, split ? split : 0xFFFFFFFFu, work,
                                                                   work_count, pairs, gcount);
-  return 2;
+  return launched;
 }
 
 size_t invert_smem_limit() { return 200 * 1024; }

@@ -859,3 +859,46 @@ def test_cache_snapshot_shorter_than_the_inputs(oracle, pool_tokens):
     compare_selection(oracle, prob, "block", b, rows, BF16_RTOL)
     print(f"snapshot of {pool_tokens} tokens: exact={ex} near-tie={near} recall={rec:.6f}")
     assert rec >= 0.999 and ex + near == len(pos)
+
+
+def test_decode_loop_replays_one_graph(oracle):
+    """A decode loop through the C ABI with DEVICE buffers (same pointers, same Q, one key appended per step): from the
+    third step on hisa_cuda_hisa_select replays one captured CUDA graph whose kernels read the sequence length from
+    device memory. Every step must equal a fresh context's plain call on the same prefix, bit for bit, and the block
+    summaries must stay those of a batch build — including across the step where the block count crosses a kernel-variant
+    boundary (1024 blocks) and across a reallocation of the key buffer."""
+    L0, B, m, k, steps = 131072 - 6, 128, 64, 2048, 12          # crosses M = 1024 -> 1025 at step 7
+    rows = np.full(64, 2 ** 31 - 1, np.uint32)                  # streaming position: always the newest token
+    prob, qb, kb = _numpy_problem(oracle, L0 + steps, rows, 91, B, m, k)
+    cfg = capi.make_config(B, m, k, 64, 128, capi.DTYPE_BF16)
+    with capi.Indexer(cfg, 0) as ix, capi.Indexer(cfg, 0) as ref:
+        ix.upload_keys(kb[:L0])
+        ix.pool_build()
+        dq, dw, dp = ix.device_alloc(qb.nbytes), ix.device_alloc(prob.gates.nbytes), ix.device_alloc(rows.nbytes)
+        d_idx, d_cnt, d_cand = ix.device_alloc(64 * k * 4), ix.device_alloc(64 * 4), ix.device_alloc(64 * 4)
+        d_key = ix.device_alloc(steps * 128 * 2)
+        ix.memcpy(dq, qb, qb.nbytes), ix.memcpy(dw, prob.gates, prob.gates.nbytes), ix.memcpy(dp, rows, rows.nbytes)
+        ix.memcpy(d_key, kb[L0:], steps * 128 * 2)
+        launches = []
+        for s in range(steps):
+            ix.pool_append(d_key + s * 256, n=1, key_dim=128)
+            l0 = ix.launch_count()
+            ix.hisa_select_raw(dq, dw, dp, 64, d_idx, d_cnt, None, None, d_cand)
+            ix.synchronize()
+            launches.append(ix.launch_count() - l0)
+            idx, cnt, cand = np.empty((64, k), np.int32), np.empty(64, np.uint32), np.empty(64, np.uint32)
+            ix.memcpy(idx, d_idx, idx.nbytes), ix.memcpy(cnt, d_cnt, cnt.nbytes), ix.memcpy(cand, d_cand, cand.nbytes)
+            L = L0 + s + 1
+            ref.upload_keys(kb[:L])
+            want = ref.hisa_select(qb, prob.gates, rows)
+            assert np.array_equal(idx, want["idx"]) and np.array_equal(cnt, want["count"]), f"step {s} (L={L}) differs"
+            assert np.array_equal(cand, want["cand"])
+        sums, counts, pooled = ix.pool_read()
+    osums, ocounts, opooled = oracle.pool_build(prob.keys, B)
+    assert counts.tolist() == ocounts.tolist() and np.array_equal(sums, osums) and np.array_equal(pooled, opooled)
+    assert len(set(launches)) <= 3, launches   # the same kernel sequence every step, replayed or not
+    # the last step against the oracle
+    prob.positions = np.full(64, L0 + steps - 1, np.uint32)
+    got = {"idx": idx, "count": cnt, "cand": cand, "blocks": want["blocks"], "nblocks": want["nblocks"]}
+    ex, near, rec = compare_selection(oracle, prob, "hisa", got, np.arange(64), BF16_RTOL)
+    assert rec >= 0.999
