@@ -7,5 +7,5 @@ tail -5 gpurun_out/pytest_gpu.log
 timeout 600 python bench.py > gpurun_out/bench_default.log 2> gpurun_out/bench_default.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.log 2> gpurun_out/bench_reference.err; echo "ref rc=$?"
 timeout 600 python bench.py --dtype fp8 > gpurun_out/bench_fp8.log 2> gpurun_out/bench_fp8.err; echo "fp8 rc=$?"
-timeout 900 python scripts/bench_configs.py > gpurun_out/bench_configs.log 2>&1; echo "configs rc=$?"
+
 tail -c 3000 gpurun_out/bench_default.log; tail -c 1500 gpurun_out/bench_reference.log

@@ -40,7 +40,7 @@ subprocess.run(["cp", os.path.join(root, "gpurun_out", "launches.csv"), os.path.
 
 # 2. full captures -> short counter tables
 for rep, name in (("prof_score_tc.ncu-rep", "score_tc"), ("prof_score_tc_fp8.ncu-rep", "score_tc_fp8"),
-                  ("prof_select.ncu-rep", "select")):
+                  ("prof_select.ncu-rep", "select"), ("prof_pool.ncu-rep", "pool")):
     path = os.path.join(root, "gpurun_out", rep)
     if not os.path.exists(path):
         continue
@@ -71,4 +71,11 @@ for rep, key, summ in (("prof_score_tc.ncu-rep", "traffic_score_tc_stage2.json",
                "dram_bytes_per_launch": rd + wr, "source": f"profiles/{tag}_{summ}_ncu_full_summary.txt"},
               open(os.path.join(out, key), "w"), indent=1)
     print(rep, "stage-2 DRAM traffic per launch: %.3f GB" % ((rd + wr) / 1e9))
+# 4. racecheck over the selection kernels alone (no TMA / tcgen05 kernel in the process)
+rc = os.path.join(root, "gpurun_out", "racecheck_select_only.log")
+if os.path.exists(rc):
+    with open(os.path.join(out, f"{tag}_racecheck_select_only.txt"), "w") as f:
+        f.write("compute-sanitizer --tool racecheck --racecheck-report analysis python -m pytest tests/test_gpu_parity.py -m gpu "
+                "-k 'top_k_on_given_scores or select_blocks_on_given'  (scripts/profile.sh; only select_* kernels launch)\n\n")
+        f.write(open(rc).read())
 print(open(os.path.join(out, f"{tag}_launches_summary.txt")).read())
