@@ -379,6 +379,12 @@ struct ScoreJob {
   const float* a_scale = nullptr;
 };
 
+// HISA_TC_ATMEM=1 (bf16 keys and queries, one segment each): the token scorer multiplies the key tile from tensor memory,
+// in groups of three queries. Measured slower than the shared-memory-operand form (score_tc.cu), hence opt-in.
+bool token_scorer_uses_tmem_tile(const hisa_cuda_ctx* ctx) {
+  return !ctx->fp8 && ctx->nseg_k == 1 && ctx->nseg_q == 1 && env_u32("HISA_TC_ATMEM", 0) != 0;
+}
+
 int run_scorer(hisa_cuda_ctx* ctx, const ScoreJob& j) {
   ScoreArgs a{};
   uint32_t* sc = ctx->scalars.as<uint32_t>();
@@ -400,6 +406,7 @@ int run_scorer(hisa_cuda_ctx* ctx, const ScoreJob& j) {
   a.fp8 = j.a8 ? 1u : 0u;
   a.a_scale = j.a_scale;
   a.epi_sleep_ns = env_u32("HISA_TC_EPI_SLEEP", 0);
+  a.a_tmem = (!j.a8 && a.nseg_a == 1 && a.nseg_b == 1 && token_scorer_uses_tmem_tile(ctx)) ? 1u : 0u;
   a.producers = std::min<uint32_t>(std::max<uint32_t>(env_u32("HISA_TC_PRODUCERS", j.a8 ? 2 : 3), 1), 3);
   a.stats = nullptr;
   if (ctx->profiling && ctx->stall_stats) {
@@ -707,13 +714,18 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
         // prefill sizes (stage 2 7.44 -> 7.22 ms, CTA balance 0.975 -> 0.988; 64 costs more in tile reloads than it
         // balances), at most 16 queries for calls of <= 2048 rows, where one forced-block list was a large share of an
         // SM's whole work (decode: longest CTA 61K cycles against a mean of 28K before the split).
-        const uint32_t split = nq <= 2048 ? env_u32("HISA_LIST_SPLIT", 4u * kGroupQ) : env_u32("HISA_LIST_SPLIT_BIG", 128u);
+        // (whole MMA groups per item: groups are 3 queries when the scorer multiplies the tile from tensor memory)
+        const uint32_t gq = token_scorer_uses_tmem_tile(ctx) ? 3u : uint32_t(kGroupQ);
+        const uint32_t split =
+            nq <= 2048 ? env_u32("HISA_LIST_SPLIT", 4u * gq) : env_u32("HISA_LIST_SPLIT_BIG", gq == 3u ? 126u : 128u);
         const uint64_t pairs_chunk = uint64_t(chunk_list) * S;
         const uint64_t items_cap =
             uint64_t(nchunks) * (std::min<uint64_t>(M, pairs_chunk) + (split ? pairs_chunk / split : 0)) * spb;
         HISA_TRY(ensure(ctx, ctx->work, size_t(items_cap) * sizeof(WorkItem)));
         HISA_TRY(ensure(ctx, ctx->pairs, size_t(nchunks) * chunk_list * S * sizeof(uint2)));
         HISA_TRY(ensure(ctx, ctx->cand, size_t(nq) * cand_cols * 4));
+        // (graph replay: the variant must not depend on the current length)
+        const uint32_t topk_cap = uint32_t(ctx->dyn ? cand_cols : std::min<uint64_t>(cand_cols, L));
         const size_t inv_words = invert_global_words(uint32_t(nq), chunk_list, M);
         if (inv_words) HISA_TRY(ensure(ctx, ctx->inv_scratch, inv_words * sizeof(uint32_t)));
         uint32_t* sc = ctx->scalars.as<uint32_t>();
@@ -766,8 +778,7 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
           s.out_count = cnt_dst;
           s.out_cand = cand_dst;
           place(s, q0);
-          // (graph replay: the variant must not depend on the current length)
-          count_launches(ctx, launch_select(s, uint32_t(nq), uint32_t(ctx->dyn ? cand_cols : std::min<uint64_t>(cand_cols, L)), ctx->stream));
+          count_launches(ctx, launch_select(s, uint32_t(nq), topk_cap, ctx->stream));
           HISA_TRY(check_launch(ctx, "top-k"));
         }
       }

@@ -57,6 +57,7 @@ struct ScoreArgs {
   uint32_t a_rows;             // rows that exist in the A operand (rows beyond read as zero)
   uint32_t fp8;                // operands are e4m3 bytes [rows, 128] (kind::f8f6f4); nseg_a = nseg_b = 1
   const float* a_scale;        // fp8: per-row dequantisation scale of the A operand (may be null = 1)
+  uint32_t a_tmem;             // bf16, one segment each: multiply the tile from tensor memory (groups of 3 queries)
   uint32_t producers;          // TMA producer warps that take part (1..3)
   uint32_t epi_sleep_ns;       // nanosleep between polls of the epilogue warps' accumulator barrier (0 = spin)
   unsigned long long* stats;   // optional [kScoreStats] role-level stall cycles, summed over CTAs (may be null)

@@ -52,28 +52,27 @@ constexpr int kMetaSlots = 8;
 constexpr int kUnitSlots = 4;
 constexpr uint32_t kAHalfBytes = kTileRows * 128;      // one 64-element K-half of one A segment: 16 KB
 constexpr uint32_t kQBoxBytes = kHeads * 128;          // one query, one K-half: 8 KB
-constexpr uint32_t kBChunkBytes = kGroupQ * kQBoxBytes;  // 32 KB
 constexpr uint32_t kGateRowBytes = kHeads * 4;         // 256 B
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kAccCols = kGroupQ * kHeads;        // 256
+constexpr uint32_t kATmemCols = 64;                    // one bf16 key tile in tensor memory: 128 lanes x 64 columns
 
 constexpr uint32_t kFlagFirst = 1u, kFlagLast = 2u, kFlagTerminate = 4u;
 
 // Per-group descriptor handed from the producer to the MMA and epilogue warps through shared memory.
 struct GroupMeta {
-  uint32_t qrow[kGroupQ];  // +0   output row of each query of the group
-  uint32_t col[kGroupQ];   // +16  output column of lane 0
+  uint32_t qrow[4];        // +0   output row of each query of the group (3 or 4 in use)
+  uint32_t col[4];         // +16  output column of lane 0
   uint32_t word;           // +32  nvalid | flags << 8 | valid_rows << 16
   uint32_t pad[3];
 };
 static_assert(sizeof(GroupMeta) == 48, "GroupMeta fields are read by byte offset");
 
-template <int NSEG_A, int ABUF, int NST, int KH>
+template <int NSEG_A, int ABUF, int NST, int KH, int GQ>
 struct SmemLayout {
   static constexpr uint32_t a_off = 0;
   static constexpr uint32_t b_off = a_off + ABUF * NSEG_A * KH * kAHalfBytes;
-  static constexpr uint32_t w_off = b_off + NST * kBChunkBytes;
-  static constexpr uint32_t meta_off = w_off + kMetaSlots * kGroupQ * kGateRowBytes;
+  static constexpr uint32_t w_off = b_off + NST * GQ * kQBoxBytes;
+  static constexpr uint32_t meta_off = w_off + kMetaSlots * GQ * kGateRowBytes;
   static constexpr uint32_t unit_off = meta_off + kMetaSlots * sizeof(GroupMeta);
   static constexpr uint32_t bar_off = unit_off + kUnitSlots * sizeof(WorkItem);
   // barriers: b_full[NST] b_empty[NST] a_full[ABUF] a_empty[ABUF] t_full[2] t_empty[2] u_full[4] u_empty[4]
@@ -131,7 +130,18 @@ struct RowSum {
 // row, so a segment is a single K slab (KH = 1) where bf16 needs two (KH = 2), and a group needs one 32 KB query
 // chunk instead of two; the per-key dequantisation scale multiplies the finished row sum (scale > 0 commutes with
 // the ReLU), the per-(query, head) scale is part of the gate.
-template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8, bool STATS>
+// ATM: the key tile (A operand) is multiplied from TENSOR MEMORY. The tile still arrives by TMA in one shared-memory
+// staging buffer; the MMA thread moves it with eight tcgen05.cp (128 rows x 32 bytes each) into 64 TMEM columns and every
+// MMA of the item reads it there, so per K = 16 step the tensor core fetches only the query operand from shared memory
+// (N x 32 bytes instead of (128 + N) x 32 bytes: the shared-memory port is this kernel's wall). 512 TMEM
+// columns = 2 accumulators + 2 tile buffers, so the accumulators shrink to 192 columns: groups of THREE queries. The
+// staging buffer is free again as soon as the copies have run, which leaves room for a deeper query ring (NST).
+// tools/umma_ts_check.cu holds this operand path against the shared-memory form bit for bit.
+// MEASURED (C3, same box, A/B): stage 2 7.22 ms against 6.92 ms for the shared-memory form, flat scorer 42 vs 40 ms: the
+// N = 192 products issue at ~132 cycles each next to the epilogue's tcgen05.ld traffic (103 in isolation), which costs
+// more than the lighter shared-memory port gives back. The variant is therefore OPT-IN (HISA_TC_ATMEM=1) and kept under
+// test (tests/test_gpu_parity.py::test_tmem_tile_variant_matches) as the measured alternative.
+template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8, bool ATM, bool STATS>
 __global__ void __launch_bounds__(kTcThreads, 1)
 score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, ScoreArgs a) {
   // producer warps: three keep up with two 32 KB chunks per group (bf16); with one chunk per group (fp8) two are
@@ -140,7 +150,13 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   constexpr int KH = FP8 ? 1 : 2;                     // 128-byte K slabs per operand segment
   constexpr int KBOX = FP8 ? 128 : 64;                // elements per slab
   constexpr uint32_t kASegBytes = KH * kAHalfBytes;   // one A segment: 16 KB (fp8) / 32 KB (bf16)
-  using L = SmemLayout<NSEG_A, ABUF, NST, KH>;
+  constexpr int GQ = ATM ? 3 : kGroupQ;               // queries per group
+  constexpr int GPB = 32 / GQ;                        // groups whose (row, col) pairs one warp-wide load fetches
+  constexpr uint32_t kBChunkBytes = GQ * kQBoxBytes;  // one K slab of a group's queries: 32 KB (24 KB with ATM)
+  constexpr uint32_t kAccCols = GQ * kHeads;          // TMEM columns of one accumulator
+  static_assert(!ATM || (NSEG_A == 1 && !FP8 && ABUF == 1), "tile from tensor memory: one bf16 segment, one staging buffer");
+  static_assert(2 * kAccCols + (ATM ? 2 * kATmemCols : 0) <= kTmemCols, "tensor memory budget");
+  using L = SmemLayout<NSEG_A, ABUF, NST, KH, GQ>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // dynamic smem is only guaranteed 16-byte aligned: round up to the 1024 B the 128B swizzle needs
   // (pointer arithmetic on the __shared__ array keeps the address space known to the compiler: LDS/STS, not generic)
@@ -285,12 +301,12 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                              smem_u32(&a_full[a_buf]), ia * kDim + kh * KBOX, int32_t(row0));
       }
       __syncwarp();
-      const uint32_t ngroups = (item.count + kGroupQ - 1) / kGroupQ;
-      for (uint32_t gb = 0; gb < ngroups; gb += 8) {
-        // 32 lanes fetch the next 32 (row, col) entries in one coalesced load
-        const uint32_t idx = gb * kGroupQ + lane;
+      const uint32_t ngroups = (item.count + GQ - 1) / GQ;
+      for (uint32_t gb = 0; gb < ngroups; gb += GPB) {
+        // the lanes fetch the (row, col) entries of the next GPB groups in one coalesced load
+        const uint32_t idx = gb * GQ + lane;
         uint32_t prow = 0, pcol = 0;
-        if (idx < item.count) {
+        if (lane < GPB * GQ && idx < item.count) {
           if (a.list_mode) {
             const uint2 p = a.pairs[item.first + idx];
             prow = p.x;
@@ -300,16 +316,17 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             pcol = col_add;
           }
         }
-        const uint32_t gend = min(8u, ngroups - gb);
+        const uint32_t gend = min(uint32_t(GPB), ngroups - gb);
         for (uint32_t gi = 0; gi < gend; ++gi) {
-          uint32_t qrow[kGroupQ], qcol[kGroupQ];
+          uint32_t qrow[4], qcol[4];
+          qrow[3] = qcol[3] = 0;
 #pragma unroll
-          for (int qi = 0; qi < kGroupQ; ++qi) {
-            qrow[qi] = __shfl_sync(0xffffffffu, prow, gi * kGroupQ + qi);
-            qcol[qi] = __shfl_sync(0xffffffffu, pcol, gi * kGroupQ + qi);
+          for (int qi = 0; qi < GQ; ++qi) {
+            qrow[qi] = __shfl_sync(0xffffffffu, prow, gi * GQ + qi);
+            qcol[qi] = __shfl_sync(0xffffffffu, pcol, gi * GQ + qi);
           }
           const uint32_t gg = gb + gi;
-          const uint32_t nvalid = min(uint32_t(kGroupQ), item.count - gg * kGroupQ);
+          const uint32_t nvalid = min(uint32_t(GQ), item.count - gg * GQ);
           const uint32_t flags = (gg == 0 ? kFlagFirst : 0u) | (gg + 1 == ngroups ? kFlagLast : 0u);
           const bool mine0 = turn == pid;  // this producer issues the group's first chunk (and its meta + gates)
           if (mine0) wait_timed(&b_empty[stage], sph, st_b);  // also guards the meta/gate slot
@@ -324,9 +341,9 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             // sees them through t_full)
             const uint32_t wbar = smem_u32(&b_full[stage]);
 #pragma unroll
-            for (uint32_t qi = 0; qi < kGroupQ; ++qi)
+            for (uint32_t qi = 0; qi < uint32_t(GQ); ++qi)
               if (qi < nvalid)
-                bulk_load_1d_addr(w_smem + (ws * kGroupQ + qi) * kGateRowBytes, a.gates + uint64_t(qrow[qi]) * kHeads,
+                bulk_load_1d_addr(w_smem + (ws * GQ + qi) * kGateRowBytes, a.gates + uint64_t(qrow[qi]) * kHeads,
                                   kGateRowBytes, wbar);
           }
           __syncwarp();
@@ -343,7 +360,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 mbar_arrive_expect_tx(&b_full[stage], nvalid * kQBoxBytes + gate_bytes);
                 const uint32_t dst = b_smem + stage * kBChunkBytes;
 #pragma unroll
-                for (uint32_t qi = 0; qi < kGroupQ; ++qi)
+                for (uint32_t qi = 0; qi < uint32_t(GQ); ++qi)
                   if (qi < nvalid)
                     tma_load_2d_addr(dst + qi * kQBoxBytes, &map_b, fbar, ib * kDim + kh * KBOX,
                                      int32_t(qrow[qi] * kHeads));
@@ -391,6 +408,22 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const uint32_t idesc = FP8 ? umma_idesc_e4m3(kTileRows, nvalid * kHeads) : umma_idesc_bf16(kTileRows, nvalid * kHeads);
       const uint32_t d_tmem = tmem_base + acc * kAccCols;
       const uint64_t a_desc = a_desc0 + uint64_t(a_buf * (NSEG_A * kASegBytes >> 4));
+      // ATM: the item's tile lives in TMEM buffer (units & 1). That buffer was last read by the MMAs of item units - 2,
+      // i.e. of groups <= g - 2, and the t_empty wait above has just proved those complete (the epilogue releases an
+      // accumulator only after the commit of the group that filled it). tcgen05.cp and the tcgen05.mma that follow it
+      // run in issue order, so no wait sits between the copies and the first product.
+      const uint32_t a_tm = tmem_base + 2 * kAccCols + (units & 1u) * kATmemCols;
+      if (ATM && (flags & kFlagFirst)) {
+        if (elect_one()) {
+#pragma unroll
+          for (int kh = 0; kh < KH; ++kh)
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4)
+              tmem_cp_128x256b(a_tm + (kh * 4 + k4) * 8, a_desc + uint64_t(kh * (kAHalfBytes >> 4) + 2 * k4));
+          umma_commit(&a_empty[a_buf]);  // staging buffer reusable once the copies have read it
+        }
+        __syncwarp();
+      }
       bool first = true;
 #pragma unroll
       for (int ib = 0; ib < NSEG_B; ++ib)
@@ -410,6 +443,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 #pragma unroll
                 for (int k4 = 0; k4 < 4; ++k4) {  // 32 bytes of K per instruction: 16 bf16 or 32 e4m3
                   if (FP8) umma_f8(d_tmem, a_tile + 2 * k4, b_desc + 2 * k4, idesc, first ? 0u : 1u);
+                  else if (ATM) umma_bf16_ts(d_tmem, a_tm + (kh * 4 + k4) * 8, b_desc + 2 * k4, idesc, first ? 0u : 1u);
                   else umma_bf16(d_tmem, a_tile + 2 * k4, b_desc + 2 * k4, idesc, first ? 0u : 1u);
                   first = false;
                 }
@@ -418,7 +452,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             umma_commit(&b_empty[stage]);  // stage reusable once these MMAs have read it
             if (ib == NSEG_B - 1 && kh == KH - 1) {
               umma_commit(&t_full[acc]);
-              if (flags & kFlagLast) umma_commit(&a_empty[a_buf]);
+              if (!ATM && (flags & kFlagLast)) umma_commit(&a_empty[a_buf]);
             }
           }
           first = false;
@@ -455,6 +489,82 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     const bool b0 = lane & 1u, b1 = lane & 2u;
     const uint32_t t_full_addr = smem_u32(&t_full[set]), t_empty_addr = smem_u32(&t_empty[set]);
     uint32_t vx[16], vy[16];
+    if constexpr (ATM) {
+      // Groups of three queries: the two warps of a (set, quarter) split the group's twelve fragments six and six. Warp
+      // half 0 reduces query 0 and the first row half (TMEM lanes +0..15) of query 1, warp half 1 the second row half of
+      // query 1 and query 2: row halves are different key rows, so nothing is combined across warps.
+      const uint32_t half = (warp >> 2) & 1u;
+      const uint32_t qf = half * 2u;                                  // the query this warp reduces completely
+      const uint32_t t_base = tmem_base + ((quarter * 32u) << 16) + set * kAccCols;
+      const uint32_t t_full_q = t_base + qf * kHeads;                 // its columns
+      const uint32_t t_half_q = t_base + kHeads + ((half * 16u) << 16);  // query 1, this warp's row half
+      const uint32_t w_base = smem_u32(s_w) + (lane & 3u) * 16u;
+      const bool half_lane = ((lane >> 1) & 1u) == half;              // lanes that end up with a row of the half query
+      for (uint32_t g = set;; g += 2) {
+        const uint32_t ws = g % kMetaSlots;
+        mbar_wait_addr_sleep(t_full_addr, (g >> 1) & 1u, a.epi_sleep_ns);
+        const uint32_t maddr = meta_base + ws * uint32_t(sizeof(GroupMeta));
+        const uint32_t word = lds_u32(maddr + 32);
+        if ((word >> 8) & kFlagTerminate) break;
+        const uint32_t nvalid = word & 0xFFu;
+        const bool row_ok = row < (word >> 16);
+        __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the spin loop
+        tc_fence_after();
+        const bool full_ok = qf < nvalid, half_ok = 1u < nvalid;
+        const uint32_t waddr = w_base + ws * (GQ * kGateRowBytes);
+        float4 gw[4];
+        float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+        RowSum f;
+        float* dst_full = nullptr;
+        if (full_ok) {
+          tmem_ld_16x128b_x8(t_full_q, vx);                               // F(qf, 0, 0)
+#pragma unroll
+          for (int h = 0; h < 4; ++h) gw[h] = lds_f4(waddr + qf * kGateRowBytes + h * 64);
+          dst_full = a.out + uint64_t(lds_u32(maddr + qf * 4)) * a.out_stride + lds_u32(maddr + 16 + qf * 4) + row;
+          tmem_ld_wait();
+          tmem_ld_16x128b_x8(t_full_q + 32, vy);                          // F(qf, 0, 1)
+          reduce_frag(vx, gw[0], gw[1], a0, a1);
+          tmem_ld_wait();
+          tmem_ld_16x128b_x8(t_full_q + (16u << 16), vx);                 // F(qf, 1, 0)
+          reduce_frag(vy, gw[2], gw[3], a0, a1);
+          tmem_ld_wait();
+          tmem_ld_16x128b_x8(t_full_q + (16u << 16) + 32, vy);            // F(qf, 1, 1)
+          reduce_frag(vx, gw[0], gw[1], a2, a3);
+          tmem_ld_wait();
+          if (half_ok) tmem_ld_16x128b_x8(t_half_q, vx);                  // F(1, half, 0)
+          reduce_frag(vy, gw[2], gw[3], a2, a3);
+          f.step1(a0, a1, a2, a3, b0);
+        } else if (half_ok) {
+          tmem_ld_16x128b_x8(t_half_q, vx);
+        }
+        if (half_ok) {
+#pragma unroll
+          for (int h = 0; h < 4; ++h) gw[h] = lds_f4(waddr + kGateRowBytes + h * 64);
+          a0 = a1 = make_float2(0.f, 0.f);
+          tmem_ld_wait();
+          tmem_ld_16x128b_x8(t_half_q + 32, vy);                          // F(1, half, 1)
+          if (full_ok) f.step2(b1);
+          reduce_frag(vx, gw[0], gw[1], a0, a1);
+          tmem_ld_wait();
+        } else if (full_ok) {
+          f.step2(b1);
+        }
+        // every dot this warp needs is in registers: hand the accumulator back to the MMA warp
+        tc_fence_before();
+        __syncwarp();
+        if (elect_one()) mbar_arrive_addr(t_empty_addr);
+        if (full_ok && row_ok) *dst_full = f.result();
+        if (half_ok) {
+          reduce_frag(vy, gw[2], gw[3], a0, a1);
+          // two rows over four lanes: lane bit 0 picks the row, lane bit 1 only splits the heads
+          const float s0 = a0.x + a0.y, s1 = a1.x + a1.y;
+          float r = (b0 ? s1 : s0) + __shfl_xor_sync(0xffffffffu, b0 ? s0 : s1, 1);
+          r += __shfl_xor_sync(0xffffffffu, r, 2);
+          if (half_lane && row_ok)
+            a.out[uint64_t(lds_u32(maddr + 4)) * a.out_stride + lds_u32(maddr + 16 + 4) + row] = r;
+        }
+      }
+    } else
     for (uint32_t g = set;; g += 2) {
       const uint32_t ws = g % kMetaSlots;
       mbar_wait_addr_sleep(t_full_addr, (g >> 1) & 1u, a.epi_sleep_ns);
@@ -469,7 +579,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       tc_fence_after();
       const bool act0 = qp < nvalid;
       const bool act1 = qp + 1 < nvalid;
-      const uint32_t waddr = w_lane + ws * (kGroupQ * kGateRowBytes);
+      const uint32_t waddr = w_lane + ws * (GQ * kGateRowBytes);
       if (act0) {
         // fragment address: + 32 per column half, + 16 lanes per row half, + 64 columns for the second query
         tmem_ld_16x128b_x8(t_lane, vx);                                // F(0, 0, 0)
@@ -545,21 +655,22 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   }
 }
 
-template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8, bool STATS>
+template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8, bool ATM, bool STATS>
 void launch_instance(const ScoreArgs& args, const CUtensorMap& map_a, const CUtensorMap& map_b, int num_sms,
                      cudaStream_t stream) {
-  using L = SmemLayout<NSEG_A, ABUF, NST, FP8 ? 1 : 2>;
+  using L = SmemLayout<NSEG_A, ABUF, NST, FP8 ? 1 : 2, ATM ? 3 : kGroupQ>;
   constexpr size_t smem = L::total + 1024;  // slack for the manual 1024 B alignment
-  auto kern = score_tc_kernel<NSEG_A, NSEG_B, TERMS, ABUF, NST, FP8, STATS>;
+  static_assert(smem <= 232448, "more shared memory than an SM has");
+  auto kern = score_tc_kernel<NSEG_A, NSEG_B, TERMS, ABUF, NST, FP8, ATM, STATS>;
   smem_opt_in(reinterpret_cast<const void*>(kern), smem);
   kern<<<num_sms, kTcThreads, smem, stream>>>(map_a, map_b, args);
 }
 
-template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8 = false>
+template <int NSEG_A, int NSEG_B, uint32_t TERMS, int ABUF, int NST, bool FP8 = false, bool ATM = false>
 int launch_variant(const ScoreArgs& args, const CUtensorMap& map_a, const CUtensorMap& map_b, int num_sms,
                    cudaStream_t stream) {
-  if (args.stats) launch_instance<NSEG_A, NSEG_B, TERMS, ABUF, NST, FP8, true>(args, map_a, map_b, num_sms, stream);
-  else launch_instance<NSEG_A, NSEG_B, TERMS, ABUF, NST, FP8, false>(args, map_a, map_b, num_sms, stream);
+  if (args.stats) launch_instance<NSEG_A, NSEG_B, TERMS, ABUF, NST, FP8, ATM, true>(args, map_a, map_b, num_sms, stream);
+  else launch_instance<NSEG_A, NSEG_B, TERMS, ABUF, NST, FP8, ATM, false>(args, map_a, map_b, num_sms, stream);
   return 1;
 }
 
@@ -576,8 +687,10 @@ int launch_score_tc(const ScoreArgs& args, const CUtensorMap& map_a, const CUten
       return launch_variant<1, 1, pack_terms(1, 0, 0), 2, 5, true>(args, map_a, map_b, num_sms, stream);
     return -1;
   }
-  if (args.nseg_a == 1 && args.nseg_b == 1 && terms == pack_terms(1, 0, 0))
+  if (args.nseg_a == 1 && args.nseg_b == 1 && terms == pack_terms(1, 0, 0)) {
+    if (args.a_tmem) return launch_variant<1, 1, pack_terms(1, 0, 0), 1, 7, false, true>(args, map_a, map_b, num_sms, stream);
     return launch_variant<1, 1, pack_terms(1, 0, 0), 2, 4>(args, map_a, map_b, num_sms, stream);
+  }
   if (args.nseg_a == 2 && args.nseg_b == 1 && terms == pack_terms(3, 0, 0))
     return launch_variant<2, 1, pack_terms(3, 0, 0), 1, 4>(args, map_a, map_b, num_sms, stream);
   if (args.nseg_a == 3 && args.nseg_b == 1 && terms == pack_terms(7, 0, 0))

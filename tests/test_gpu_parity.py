@@ -178,6 +178,31 @@ def test_lattice_inputs_bit_exact(oracle, scorer, shape, tb):
         assert h["cand"][r] == want.cand[i]
 
 
+def test_tmem_tile_variant_matches(oracle, monkeypatch):
+    """HISA_TC_ATMEM=1: the token scorer reads the key tile from tensor memory (tcgen05.cp + the TMEM-operand form of
+    tcgen05.mma, groups of three queries). Same arithmetic, so lattice inputs must still match the oracle bit for bit,
+    ragged groups (list lengths not divisible by 3) and the dense flat mode included."""
+    monkeypatch.setenv("HISA_TC_ATMEM", "1")
+    L, H, d, B, m, k = 1700, 64, 128, 128, 3, 300
+    pos = np.arange(L, dtype=np.uint32)
+    prob = oracle.make_inputs("lattice", 11, L, pos, H, d, block_size=B, block_budget=m, token_budget=k)
+    q, kk = round_problem_to_bf16(prob)
+    rows = np.unique(np.concatenate([np.arange(0, L, 11), [0, 1, L - 1, k - 1, k, m * B]]))
+    with indexer_for(prob, capi.DTYPE_BF16, capi.SCORER_TENSOR) as ix:
+        ix.upload_keys(kk)
+        h = ix.hisa_select(q, prob.gates, pos)
+        f = ix.dsa_select(q, prob.gates, pos)
+    compare_selection(oracle, prob, "hisa", h, rows, 0.0, require_exact=True)
+    compare_selection(oracle, prob, "dsa", f, rows, 0.0, require_exact=True)
+    prob = oracle.make_inputs("random", 12, L, pos, H, d, block_size=B, block_budget=m, token_budget=k)
+    q, kk = round_problem_to_bf16(prob)
+    with indexer_for(prob, capi.DTYPE_BF16, capi.SCORER_TENSOR) as ix:
+        ix.upload_keys(kk)
+        h = ix.hisa_select(q, prob.gates, pos)
+    _, _, rec = compare_selection(oracle, prob, "hisa", h, rows, BF16_RTOL)
+    assert rec >= 0.999
+
+
 @pytest.mark.parametrize("ffl,fib", [(False, False), (True, True)])
 def test_lattice_forced_block_policies(oracle, ffl, fib):
     L = 1024
