@@ -66,8 +66,9 @@ def load_peaks():
     if os.path.exists(path):
         p = json.load(open(path))
         return {"tflops": float(p.get("bf16_tflops_sustained", p.get("bf16_tflops", 1400.0))),
+                "tflops_burst": float(p.get("bf16_tflops", 0.0)) or None,
                 "hbm_gbs": float(p.get("hbm_gbs", 6650.0)), "source": "measured (MEASURED_PEAKS.json, sustained bf16)"}
-    return {"tflops": 1400.0, "hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+    return {"tflops": 1400.0, "tflops_burst": None, "hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
 # ------------------------------------------------------------------------------------------- clocks
@@ -577,6 +578,11 @@ def run_b200(a, rank, world, local_rank):
                 "achieved": achieved, "peak": peaks["tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["tflops"], "traffic": traffic, "peak_source": peaks["source"],
                 "flops_per_launch": flops_s2, "kernel_ms": k_ms}
+    # the kernel runs inside a long step under sw_power_cap, so the sustained peak is the denominator of `frac`; the burst
+    # figure (a kernel timed alone, cold chip) is quoted beside it
+    if not fp8 and peaks.get("tflops_burst"):
+        roofline["peak_burst"] = peaks["tflops_burst"]
+        roofline["frac_of_burst_peak"] = achieved / peaks["tflops_burst"]
     per_call = {kk: (vv / a.steps if kk.endswith("_ms") else vv) for kk, vv in stages.items()
                 if kk != "stalls"}
     # ---- every stage against the roofline that bounds it (algorithmic work / CUDA-event time)
@@ -600,6 +606,9 @@ def run_b200(a, rank, world, local_rank):
         "top_k": stage_roof(per_call["top_k_ms"], "hbm", 4.0 * cand_sum + 4.0 * nq * k,
                             "candidate scores read + [Q,k] int32 indices written"),
     }
+    # the whole step (every stage, launch gaps included) against the same tensor peak: algorithmic FLOPs of both scorers
+    stage_rooflines["whole_step"] = stage_roof(ms_step, "tensor", flops_s2 + 2.0 * d * H * elig_sum,
+                                               "(2*d*H*sum_t|Omega_t| + 2*d*H*sum_t eligible blocks) / ms_per_step")
     pool_bytes = float(L) * d * eb + (4.0 * L if fp8 else 0.0) + ((L + B - 1) // B) * d * (8.0 + 4.0)
     stage_rooflines["pool_build"] = stage_roof(pool_ms, "hbm", pool_bytes,
                                                "keys read once (+ per-key scales for e4m3), f64 sums + bf16 hi|lo pooled keys "
@@ -638,7 +647,11 @@ def run_b200(a, rank, world, local_rank):
         fk_ms = fstages["score_tokens_ms"] / max(fstages["calls"], 1)
         flat = {"ms_per_step": flat_step, "queries_per_s": Q / (flat_step * 1e-3), "hisa_speedup": flat_step / ms_step,
                 "scorer_ms": fk_ms, "top_k_ms": fstages["top_k_ms"] / max(fstages["calls"], 1),
-                "scorer_tflops": 2.0 * d * H * prefix / (fk_ms * 1e-3) / 1e12 if fk_ms > 0 else None}
+                "scorer_tflops": 2.0 * d * H * prefix / (fk_ms * 1e-3) / 1e12 if fk_ms > 0 else None,
+                # the flat arm's top-k over whole prefixes is a weaker kernel than its scorer: the scorer-only ratio is the
+                # speed-up that does not lean on it (it tracks the FLOP ratio of the two indexers)
+                "hisa_speedup_scorers_only": fk_ms / per_call["score_tokens_ms"] if per_call["score_tokens_ms"] > 0 else None,
+                "flop_ratio_flat_over_hisa": 2.0 * d * H * prefix / (flops_s2 + 2.0 * d * H * elig_sum)}
 
     # ---- the step after the path: sparse_attend over the [Q, k] indices just selected.
     # Shared-KV latents [L, d_model] bf16 (16 MiB at 64K x 128: L2-resident), one state vector per query.
