@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
 constexpr int kWarpSelThreads = 256;
 
 template <int KPL>
-__global__ void __launch_bounds__(kWarpSelThreads) select_warp_kernel(SelectArgs a, uint32_t rows) {
+__global__ void __launch_bounds__(kWarpSelThreads, KPL <= 16 ? 5 : 4) select_warp_kernel(SelectArgs a, uint32_t rows) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t row = blockIdx.x * (kWarpSelThreads / 32) + (threadIdx.x >> 5);
   if (row >= rows) return;  // warp-uniform
@@ -367,32 +367,84 @@ __global__ void __launch_bounds__(kWarpSelThreads) select_warp_kernel(SelectArgs
     key[j] = k;
   }
   const uint32_t lo = __reduce_min_sync(FULL, kmin), hi = __reduce_max_sync(FULL, kmax);
-  uint32_t T = hi, kk = keep;
-  bool all_ties = false;  // the descent stopped early: every key equal to T is kept
+  // keep-th largest key: range-adaptive 8-bit radix levels on a warp-private shared-memory histogram (256 bins over the
+  // range the threshold is known to lie in), finished by ranking the survivors with shuffles once 32 or fewer remain.
+  // Distinct scores take one level (n / 256 keys fall into the threshold bin) and the ranking; the bitwise descent this
+  // replaces paid ~3 instructions per key for each of ~log2(n) + 4 bits (1670 warp instructions per 512-score row).
+  __shared__ __align__(16) uint32_t whist[kWarpSelThreads / 32][256];
+  __shared__ uint32_t wlist[kWarpSelThreads / 32][33];  // [32] = fill counter
+  uint32_t T = hi, kk = keep;  // after the search: kk = how many keys EQUAL to T are still to take
+  const bool all_ties = false;
   if (lo != hi) {
-    const int top = 31 - __clz(lo ^ hi);
-    uint32_t prefix = hi & ~((2u << top) - 1u);  // bits above `top` are common to all candidates
-    for (int bit = top; bit >= 0; --bit) {
-      const uint32_t want = (prefix >> bit) | 1u;
-      uint32_t c = 0;
-#pragma unroll
-      for (int j = 0; j < KPL; ++j) c += ((key[j] >> bit) == want) ? 1u : 0u;
-      c = __reduce_add_sync(FULL, c);
-      if (c == kk) {
-        // the keys under this prefix are exactly the ones still to take: the threshold is their minimum and the
-        // remaining bits need no descent (distinct scores reach this point after ~log2(n) + a few bits)
-        uint32_t m = 0xFFFFFFFFu;
-#pragma unroll
-        for (int j = 0; j < KPL; ++j)
-          if ((key[j] >> bit) == want) m = min(m, key[j]);
-        prefix = __reduce_min_sync(FULL, m);
-        all_ties = true;
+    uint32_t* hist = whist[threadIdx.x >> 5];
+    uint32_t* list = wlist[threadIdx.x >> 5];
+    uint32_t l = lo, h = hi, in_range = n;
+    for (;;) {
+      if (l == h) {  // every remaining key is the threshold value
+        T = l;
         break;
       }
-      if (c > kk) prefix |= 1u << bit;
-      else kk -= c;
+      const uint32_t span = h - l;
+      if (in_range <= 32u) {
+        // lane i receives one of the keys of [l, h], in any order (non-candidates are key 0: 0 - l wraps past every span)
+        if (lane == 0) list[32] = 0u;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < KPL; ++j)
+          if (key[j] - l <= span) list[atomicAdd(&list[32], 1u)] = key[j];
+        __syncwarp();
+        const uint32_t mine = lane < in_range ? list[lane] : 0u;
+        uint32_t g = 0, eq = 0;
+        for (uint32_t i = 0; i < in_range; ++i) {
+          const uint32_t o = __shfl_sync(FULL, mine, int(i));
+          g += o > mine;
+          eq += o == mine;
+        }
+        const bool is_t = lane < in_range && g < kk && kk <= g + eq;  // true for every lane holding the threshold value
+        const int src = __ffs(__ballot_sync(FULL, is_t)) - 1;
+        T = __shfl_sync(FULL, mine, src);
+        kk -= __shfl_sync(FULL, g, src);
+        break;
+      }
+      const uint32_t nb = 32 - __clz(span);
+      const uint32_t shift = nb > 8u ? nb - 8u : 0u;
+      reinterpret_cast<uint4*>(hist)[lane * 2] = make_uint4(0u, 0u, 0u, 0u);
+      reinterpret_cast<uint4*>(hist)[lane * 2 + 1] = make_uint4(0u, 0u, 0u, 0u);
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) {
+        const uint32_t d = key[j] - l;
+        if (d <= span) atomicAdd(&hist[d >> shift], 1u);
+      }
+      __syncwarp();
+      // lane owns bins 8 lane .. 8 lane + 7; suffix sums over lanes find the bin that holds the kk-th largest key
+      const uint4 ha = reinterpret_cast<const uint4*>(hist)[lane * 2], hb4 = reinterpret_cast<const uint4*>(hist)[lane * 2 + 1];
+      const uint32_t hb[8] = {ha.x, ha.y, ha.z, ha.w, hb4.x, hb4.y, hb4.z, hb4.w};
+      const uint32_t loc = ha.x + ha.y + ha.z + ha.w + hb4.x + hb4.y + hb4.z + hb4.w;
+      uint32_t inc = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_down_sync(FULL, inc, o);
+        if (lane + o < 32u) inc += y;
+      }
+      const uint32_t above = inc - loc;  // keys in bins owned by higher lanes
+      const bool owner = above < kk && kk <= above + loc;
+      uint32_t c = above, bj = 7u, cnt = hb[7];
+#pragma unroll
+      for (int jj = 7; jj > 0; --jj) {
+        if (bj == uint32_t(jj) && c + hb[jj] < kk) {
+          c += hb[jj];
+          bj = uint32_t(jj - 1);
+          cnt = hb[jj - 1];
+        }
+      }
+      const int src = __ffs(__ballot_sync(FULL, owner)) - 1;  // exactly one lane owns the threshold bin
+      const uint32_t bin = __shfl_sync(FULL, lane * 8u + bj, src);
+      kk -= __shfl_sync(FULL, c, src);
+      in_range = __shfl_sync(FULL, cnt, src);
+      l += bin << shift;
+      h = min(h, l + ((1u << shift) - 1u));
     }
-    T = prefix;
   }
   uint32_t cG = 0, cE = 0;
 #pragma unroll
@@ -418,17 +470,28 @@ __global__ void __launch_bounds__(kWarpSelThreads) select_warp_kernel(SelectArgs
   }
   const uint32_t lt = (1u << lane) - 1u;
   uint32_t o_run = add_first, e_run = 0;
+  if (need == totE) {  // every key equal to T is kept (the usual case): one ballot per 32 keys
 #pragma unroll
-  for (int j = 0; j < KPL; ++j) {
-    if (32u * j >= n) break;  // warp-uniform
-    const bool g = key[j] > T, e = key[j] == T;
-    const uint32_t be = __ballot_sync(FULL, e);
-    const uint32_t erank = e_run + __popc(be & lt);
-    const bool emit = g || (e && erank >= skip && erank < skip + need);
-    const uint32_t bm = __ballot_sync(FULL, emit);
-    if (emit) orow[o_run + __popc(bm & lt)] = position_of(lane + 32u * j);
-    o_run += __popc(bm);
-    e_run += __popc(be);
+    for (int j = 0; j < KPL; ++j) {
+      if (32u * j >= n) break;  // warp-uniform
+      const bool emit = key[j] >= T;
+      const uint32_t bm = __ballot_sync(FULL, emit);
+      if (emit) orow[o_run + __popc(bm & lt)] = position_of(lane + 32u * j);
+      o_run += __popc(bm);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+      if (32u * j >= n) break;  // warp-uniform
+      const bool g = key[j] > T, e = key[j] == T;
+      const uint32_t be = __ballot_sync(FULL, e);
+      const uint32_t erank = e_run + __popc(be & lt);
+      const bool emit = g || (e && erank >= skip && erank < skip + need);
+      const uint32_t bm = __ballot_sync(FULL, emit);
+      if (emit) orow[o_run + __popc(bm & lt)] = position_of(lane + 32u * j);
+      o_run += __popc(bm);
+      e_run += __popc(be);
+    }
   }
   const uint32_t count = totG + need + add_first + add_last;
   if (lane == 0) {
