@@ -63,7 +63,8 @@ struct hisa_cuda_ctx {
   // sequence, hisa/hisa.hpp:16-21): eligibility is clipped to pool_blocks and the keys are not re-pooled
   bool pool_external = false;
   uint64_t pool_blocks = 0;
-  DevBuf key_op, key_raw, key_scale, sums, counts, pooled_op;
+  DevBuf key_op, key_raw, key_scale, sums, counts, pooled_op, pool_scale;
+  bool pool8 = false;  // e4m3 storage + tensor-core scorer: pooled keys are four e4m3 terms + a power-of-two scale per block
 
   // per-call workspace
   DevBuf q_raw, q_op, gates_raw, gates_pad, pos, J, sel, nsel, work, pairs, scalars, cand, flat, out_idx, out_count,
@@ -339,6 +340,8 @@ int prepare_inputs(hisa_cuda_ctx* ctx, const void* queries, const float* gates, 
   // operands
   if (ctx->q_zero_copy) {
     out->q_op = static_cast<const __nv_bfloat16*>(q_dev);
+  } else if (ctx->pool8) {
+    out->q_op = nullptr;  // every scorer reads the e4m3 bytes
   } else {
     HISA_TRY(ensure(ctx, ctx->q_op, size_t(Q) * kHeads * ctx->nseg_q * kDim * sizeof(__nv_bfloat16)));
     count_launches(ctx, launch_convert_rows(q_dev, st, Q, H, d, ctx->nseg_q, ctx->q_op.as<__nv_bfloat16>(), kHeads,
@@ -421,8 +424,8 @@ int run_scorer(hisa_cuda_ctx* ctx, const ScoreJob& j) {
   } else {
     CUtensorMap map_a, map_b;
     if (j.a8) {
-      a.nseg_a = a.nseg_b = 1;
-      HISA_TRY(make_map(ctx, &map_a, j.a8, j.a_rows, kDim, kTileRows, true));
+      a.nseg_b = 1;
+      HISA_TRY(make_map(ctx, &map_a, j.a8, j.a_rows, uint64_t(a.nseg_a) * kDim, kTileRows, true));
       HISA_TRY(make_map(ctx, &map_b, j.q8, j.nq * kHeads, kDim, kHeads, true));
     } else {
       HISA_TRY(make_map(ctx, &map_a, j.a_op, j.a_rows, uint64_t(j.nseg_a) * kDim, kTileRows));
@@ -513,11 +516,22 @@ int run_score_blocks(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, uint64_
                                               ctx->cfg.block_size, ntiles, ctx->work.as<WorkItem>(), sc, sc + 1,
                                               ctx->dyn ? ctx->dlen.as<uint32_t>() : nullptr, sc + 2, sc + 3, ctx->stream));
   ScoreJob j{};
-  j.a_op = ctx->pooled_op.as<__nv_bfloat16>();
   j.a_rows = M;
-  j.nseg_a = ctx->nseg_p;
-  j.terms = ctx->terms_blk;
-  j.q_op = p.q_op + q0 * kHeads * ctx->nseg_q * kDim;
+  static const uint32_t terms_pool8[kMaxSeg] = {(1u << kPool8Seg) - 1u, 0, 0};
+  if (ctx->pool8) {
+    // e4m3 storage: the queries stay e4m3 bytes and meet the pooled keys as four e4m3 terms in kind::f8f6f4 (no bf16 copy
+    // of the queries); the block's power-of-two scale multiplies the finished row sum like a key's scale does in stage 2
+    j.a8 = ctx->pooled_op.as<uint8_t>();
+    j.q8 = p.q8 + q0 * kHeads * kDim;
+    j.a_scale = ctx->pool_scale.as<float>();
+    j.nseg_a = kPool8Seg;
+    j.terms = terms_pool8;
+  } else {
+    j.a_op = ctx->pooled_op.as<__nv_bfloat16>();
+    j.nseg_a = ctx->nseg_p;
+    j.terms = ctx->terms_blk;
+    j.q_op = p.q_op + q0 * kHeads * ctx->nseg_q * kDim;
+  }
   j.nq = nq;
   j.gates = p.gates + q0 * kHeads;
   j.out = ctx->J.as<float>();
@@ -1177,8 +1191,9 @@ int hisa_cuda_create(int device, const hisa_cuda_config* cfg, hisa_cuda_ctx** ou
   const bool bf16 = cfg->dtype == HISA_DTYPE_BF16;
   ctx->fp8 = cfg->dtype == HISA_DTYPE_FP8_E4M3;
   if (bf16 || ctx->fp8) {
-    // fp8: stage 1 multiplies a bf16 copy of q (e4m3 values are exact in bf16) with the bf16 hi|lo pooled keys;
-    // stage 2 and the flat scorer read the e4m3 bytes of q and k directly
+    // fp8: stage 2 and the flat scorer read the e4m3 bytes of q and k directly. Stage 1 reads the e4m3 queries too, against
+    // pooled keys stored as four e4m3 terms + a power-of-two scale per block (pool8). HISA_FP8_BLOCKS=0 or the SIMT
+    // cross-check scorer: stage 1 multiplies a bf16 copy of q (e4m3 values are exact in bf16) with bf16 hi|lo pooled keys
     ctx->nseg_k = ctx->nseg_q = 1;
     ctx->nseg_p = std::min<uint32_t>(std::max<uint32_t>(env_u32("HISA_POOL_SEGS", 2), 1), kMaxSeg);
     ctx->terms_tok[0] = 1; ctx->terms_tok[1] = ctx->terms_tok[2] = 0;
@@ -1189,6 +1204,8 @@ int hisa_cuda_create(int device, const hisa_cuda_config* cfg, hisa_cuda_ctx** ou
     ctx->terms_tok[0] = 0b111; ctx->terms_tok[1] = 0b011; ctx->terms_tok[2] = 0b001;
     for (int i = 0; i < kMaxSeg; ++i) ctx->terms_blk[i] = ctx->terms_tok[i];
   }
+  ctx->pool8 = ctx->fp8 && cfg->scorer != HISA_SCORER_SIMT && env_u32("HISA_FP8_BLOCKS", 1) != 0;
+  if (ctx->pool8) ctx->nseg_p = 2;  // four e4m3 terms take the bytes of two bf16 segments: one buffer layout for both forms
   ctx->q_zero_copy = bf16 && cfg->num_heads == uint32_t(kHeads) && cfg->dim == uint32_t(kDim);
   ctx->chunk_dense = std::max<uint32_t>(env_u32("HISA_CHUNK_DENSE", 128), 4);
   ctx->chunk_list = std::max<uint32_t>(env_u32("HISA_CHUNK_LIST", 512), 4);
@@ -1205,7 +1222,8 @@ int hisa_cuda_destroy(hisa_cuda_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   drop_graph(ctx);
   release(ctx->dlen);
-  for (DevBuf* b : {&ctx->key_op, &ctx->key_raw, &ctx->key_scale, &ctx->sums, &ctx->counts, &ctx->pooled_op, &ctx->q_raw, &ctx->q_op,
+  for (DevBuf* b : {&ctx->key_op, &ctx->key_raw, &ctx->key_scale, &ctx->sums, &ctx->counts, &ctx->pooled_op, &ctx->pool_scale,
+                    &ctx->q_raw, &ctx->q_op,
                     &ctx->gates_raw, &ctx->gates_pad, &ctx->pos, &ctx->J, &ctx->sel, &ctx->nsel, &ctx->work, &ctx->pairs,
                     &ctx->scalars, &ctx->cand, &ctx->flat, &ctx->out_idx, &ctx->out_count, &ctx->out_cand,
                     &ctx->generic_scores, &ctx->generic_n, &ctx->export_a, &ctx->export_b, &ctx->flag, &ctx->stats,
@@ -1281,7 +1299,7 @@ static int grow_keys(hisa_cuda_ctx* ctx, uint64_t need_tokens) {
   cap = round_up64(cap, 1024);
   const size_t row_bytes = ctx->fp8 ? size_t(kDim) : size_t(ctx->nseg_k) * kDim * sizeof(__nv_bfloat16);
   const uint64_t mcap = (cap + ctx->cfg.block_size - 1) / ctx->cfg.block_size + 1;
-  DevBuf nk, ns, nc, np, nsc;
+  DevBuf nk, ns, nc, np, nsc, npsc;
   CU_TRY(ctx, cudaMalloc(&nk.p, cap * row_bytes));
   if (ctx->fp8) {
     CU_TRY(ctx, cudaMalloc(&nsc.p, cap * sizeof(float)));
@@ -1293,6 +1311,11 @@ static int grow_keys(hisa_cuda_ctx* ctx, uint64_t need_tokens) {
   nk.cap = cap * row_bytes; ns.cap = mcap * kDim * sizeof(double); nc.cap = mcap * sizeof(uint32_t);
   np.cap = mcap * ctx->nseg_p * kDim * sizeof(__nv_bfloat16);
   CU_TRY(ctx, cudaMemsetAsync(np.p, 0, np.cap, ctx->stream));
+  if (ctx->pool8) {  // one scale per pooled row, padded to whole 128-row tiles (the scorer's epilogue reads a tile's worth)
+    npsc.cap = (mcap + kTileRows) * sizeof(float);
+    CU_TRY(ctx, cudaMalloc(&npsc.p, npsc.cap));
+    CU_TRY(ctx, cudaMemsetAsync(npsc.p, 0, npsc.cap, ctx->stream));
+  }
   if (ctx->seq_len) {
     const uint64_t M = num_blocks_of(ctx);
     CU_TRY(ctx, cudaMemcpyAsync(nk.p, ctx->key_op.p, ctx->seq_len * row_bytes, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1302,10 +1325,13 @@ static int grow_keys(hisa_cuda_ctx* ctx, uint64_t need_tokens) {
     CU_TRY(ctx, cudaMemcpyAsync(nc.p, ctx->counts.p, M * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
     CU_TRY(ctx, cudaMemcpyAsync(np.p, ctx->pooled_op.p, M * ctx->nseg_p * kDim * sizeof(__nv_bfloat16),
                                 cudaMemcpyDeviceToDevice, ctx->stream));
+    if (ctx->pool8)
+      CU_TRY(ctx, cudaMemcpyAsync(npsc.p, ctx->pool_scale.p, M * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
   }
   CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   release(ctx->key_op); release(ctx->sums); release(ctx->counts); release(ctx->pooled_op); release(ctx->key_scale);
-  ctx->key_op = nk; ctx->sums = ns; ctx->counts = nc; ctx->pooled_op = np; ctx->key_scale = nsc;
+  release(ctx->pool_scale);
+  ctx->key_op = nk; ctx->sums = ns; ctx->counts = nc; ctx->pooled_op = np; ctx->key_scale = nsc; ctx->pool_scale = npsc;
   ctx->key_cap = cap;
   return HISA_OK;
 }
@@ -1353,7 +1379,8 @@ static int pool_update(hisa_cuda_ctx* ctx, uint64_t first, uint64_t n) {
     count_launches(ctx, launch_pool_update_fp8(ctx->key_op.as<uint8_t>(), ctx->key_scale.as<float>(), first, n,
                                                ctx->cfg.block_size, ctx->cfg.pool_mode, ctx->sums.as<double>(),
                                                ctx->counts.as<uint32_t>(), ctx->pooled_op.as<__nv_bfloat16>(), ctx->nseg_p,
-                                               ctx->dlen.as<uint32_t>(), ctx->stream));
+                                               ctx->pool8 ? ctx->pool_scale.as<float>() : nullptr, ctx->dlen.as<uint32_t>(),
+                                               ctx->stream));
   else
     count_launches(ctx, launch_pool_update(ctx->key_op.as<__nv_bfloat16>(), ctx->nseg_k, first, n, ctx->cfg.block_size,
                                            ctx->cfg.dim, ctx->cfg.pool_mode, ctx->sums.as<double>(), ctx->counts.as<uint32_t>(),
@@ -1448,7 +1475,7 @@ int hisa_cuda_pool_set(hisa_cuda_ctx* ctx, const double* sums, const uint32_t* c
   }
   count_launches(ctx, launch_pool_import(s_dev, c_dev, M, d, ctx->cfg.pool_mode, ctx->sums.as<double>(),
                                          ctx->counts.as<uint32_t>(), ctx->pooled_op.as<__nv_bfloat16>(), ctx->nseg_p,
-                                         ctx->stream));
+                                         ctx->pool8 ? ctx->pool_scale.as<float>() : nullptr, ctx->stream));
   HISA_TRY(check_launch(ctx, "pool import"));
   CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // the caller's host arrays may go away after the call
   ctx->pool_external = true;

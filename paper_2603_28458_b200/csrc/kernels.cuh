@@ -21,7 +21,8 @@ constexpr int kTileRows = 128;  // operand rows per tile (UMMA M)
 constexpr int kHeads = 64;      // heads per query in the operand (padded)
 constexpr int kDim = 128;       // elements per operand segment (padded d)
 constexpr int kGroupQ = 4;      // queries per MMA group (UMMA N = 256)
-constexpr int kMaxSeg = 3;
+constexpr int kMaxSeg = 3;       // bf16 segments per operand row
+constexpr int kPool8Seg = 4;     // e4m3 terms of a pooled key (fp8 storage): 4 x 4 significant bits
 constexpr int kMaxReplicas = 7;  // peer copies of the selection output (8-GPU box: 7 peers)
 
 // position of head j inside a query's 64-float gate row. tcgen05.ld.16x128b hands the columns (heads) {4i + c : i = 0..15}
@@ -52,10 +53,10 @@ struct ScoreArgs {
   uint32_t list_mode;
   uint32_t segs_per_block;     // list mode: tiles per key block = ceil(B / 128); dense: 1
   uint32_t block_rows;         // list mode: B; dense: 128
-  uint32_t nseg_a, nseg_b;     // operand segments of the tile (A) and query (B) operands
+  uint32_t nseg_a, nseg_b;     // operand segments of the tile (A) and query (B) operands (fp8: nseg_a is 1, or 4 for pooled keys)
   uint32_t terms[kMaxSeg];     // terms[ib] = bit mask of A segments multiplied with B segment ib
   uint32_t a_rows;             // rows that exist in the A operand (rows beyond read as zero)
-  uint32_t fp8;                // operands are e4m3 bytes [rows, 128] (kind::f8f6f4); nseg_a = nseg_b = 1
+  uint32_t fp8;                // operands are e4m3 bytes [rows, nseg * 128] (kind::f8f6f4); nseg_b = 1
   const float* a_scale;        // fp8: per-row dequantisation scale of the A operand (may be null = 1)
   uint32_t a_tmem;             // bf16, one segment each: multiply the tile from tensor memory (groups of 3 queries)
   uint32_t producers;          // TMA producer warps that take part (1..3)
@@ -197,16 +198,19 @@ int launch_check_finite(const void* src, uint32_t src_type, uint64_t n, uint32_t
 int launch_check_positions(const uint32_t* pos, uint64_t n, uint32_t seq_len, uint32_t* flag, cudaStream_t stream);
 // block summaries over tokens [first, first+n): double sums, counts, pooled operand (nseg_p segments)
 // len_out (may be null): device word that receives first + n, the sequence length after the update
+// pool_scale (may be null): non-null selects the e4m3 form of the pooled operand: row b = kPool8Seg x 128 e4m3 bytes
+// t0 | t1 | t2 | t3 with pooled key = (t0 + t1 + t2 + t3) * pool_scale[b], pool_scale[b] a power of two (same bytes per row
+// as the bf16 hi | lo form, so the two share one buffer); the block scorer then runs in kind::f8f6f4 on the e4m3 queries
 int launch_pool_update(const __nv_bfloat16* key_op, uint32_t nseg_k, uint64_t first, uint64_t n, uint32_t block_size,
                        uint32_t dim, uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op,
                        uint32_t nseg_p, uint32_t* len_out, cudaStream_t stream);
 int launch_pool_update_fp8(const uint8_t* key8, const float* key_scale, uint64_t first, uint64_t n, uint32_t block_size,
                            uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op, uint32_t nseg_p,
-                           uint32_t* len_out, cudaStream_t stream);
+                           float* pool_scale, uint32_t* len_out, cudaStream_t stream);
 // installs caller-provided summaries: src_sums f64 [num_blocks, dim], src_counts [num_blocks] (device pointers)
 int launch_pool_import(const double* src_sums, const uint32_t* src_counts, uint32_t num_blocks, uint32_t dim,
                        uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op, uint32_t nseg_p,
-                       cudaStream_t stream);
+                       float* pool_scale, cudaStream_t stream);
 int launch_fill_f32(float* dst, uint64_t n, float v, cudaStream_t stream);
 int launch_pool_export(const double* sums, const uint32_t* counts, uint32_t num_blocks, uint32_t dim,
                        uint32_t pool_max, double* out_sums, double* out_pooled, cudaStream_t stream);

@@ -36,6 +36,46 @@ __device__ __forceinline__ void split_bf16(float x, int nseg, __nv_bfloat16* par
   }
 }
 
+// Pooled key of block b, column c (one thread per column, all kDim threads of the CTA call this together).
+// pool_scale == null: bf16 segments hi | lo [| lo2] of the f32 value. pool_scale != null (e4m3 storage): four e4m3 terms
+// t0 | t1 | t2 | t3 with p = (t0 + t1 + t2 + t3) * 2^e, 2^e = pool_scale[b] chosen from the row's largest magnitude so that t0
+// uses the top of the e4m3 range: each term keeps 4 significant bits of what the terms before it left over (the subtraction
+// is exact), so the row is represented to 2^-16 of its largest element, and exactly when the values need <= 15 bits (lattice
+// inputs). A power-of-two scale keeps p / 2^e and the final multiply in the scorer's epilogue exact.
+__device__ __forceinline__ void store_pooled(uint64_t b, uint32_t c, float p, __nv_bfloat16* pooled_op, uint32_t nseg_p,
+                                             float* pool_scale) {
+  if (pool_scale == nullptr) {
+    __nv_bfloat16 parts[kMaxSeg];
+    split_bf16(p, int(nseg_p), parts);
+    for (uint32_t g = 0; g < nseg_p; ++g) pooled_op[b * (uint64_t(nseg_p) * kDim) + g * kDim + c] = parts[g];
+    return;
+  }
+  __shared__ float s_max[kDim / 32];
+  float m = fabsf(p);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __syncthreads();  // s_max may still be read by a previous use in this CTA
+  if ((c & 31u) == 0) s_max[c >> 5] = m;
+  __syncthreads();
+  m = fmaxf(fmaxf(s_max[0], s_max[1]), fmaxf(s_max[2], s_max[3]));
+  // smallest power of two with m / 2^e <= 448 (the largest e4m3 value); an all-zero row keeps scale 1
+  int e = 0;
+  if (m > 0.f) {
+    frexpf(m / 448.0f, &e);                      // m / 448 = f * 2^e, f in [0.5, 1)
+    if (ldexpf(448.0f, e - 1) >= m) e -= 1;      // f == 0.5 exactly: one power less still fits
+  }
+  const float scale = ldexpf(1.0f, e);
+  if (c == 0) pool_scale[b] = scale;
+  float r = ldexpf(p, -e);
+  uint8_t* row = reinterpret_cast<uint8_t*>(pooled_op) + b * (uint64_t(kPool8Seg) * kDim);
+#pragma unroll
+  for (int g = 0; g < kPool8Seg; ++g) {
+    const uint8_t t = uint8_t(__nv_cvt_float_to_fp8(r, __NV_SATFINITE, __NV_E4M3));
+    row[g * kDim + c] = t;
+    r -= e4m3_to_float(t);
+  }
+}
+
 // dst row (o*dst_heads + h) <- src row (o*src_heads + h) for h < src_heads, zero rows otherwise;
 // columns >= src_dim are zero. One thread per (dst row, 8-column group).
 __global__ void convert_rows_kernel(const void* __restrict__ src, uint32_t src_type, uint64_t outer,
@@ -165,9 +205,7 @@ pool_update_kernel(const __nv_bfloat16* __restrict__ key_op, uint32_t nseg_k, ui
   const uint32_t cnt = uint32_t(s_hi - blk_lo);
   if (c == 0) counts[b] = cnt;
   const double p = pool_max ? acc : acc / double(cnt);
-  __nv_bfloat16 parts[kMaxSeg];
-  split_bf16(float(p), int(nseg_p), parts);
-  for (uint32_t g = 0; g < nseg_p; ++g) pooled_op[b * (uint64_t(nseg_p) * kDim) + g * kDim + c] = parts[g];
+  store_pooled(b, c, float(p), pooled_op, nseg_p, nullptr);
 }
 
 // Same accumulation for e4m3 keys with a per-key scale: the summed value is float(k8) * scale (one f32 rounding),
@@ -176,7 +214,7 @@ __global__ void __launch_bounds__(kDim)
 pool_update_fp8_kernel(const uint8_t* __restrict__ key8, const float* __restrict__ key_scale, uint64_t first, uint64_t n,
                        uint32_t block_size, uint32_t pool_max, double* __restrict__ sums,
                        uint32_t* __restrict__ counts, __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p,
-                       uint32_t* __restrict__ len_out) {
+                       float* __restrict__ pool_scale, uint32_t* __restrict__ len_out) {
   const uint64_t b = first / block_size + blockIdx.x;
   const uint32_t c = threadIdx.x;
   if (len_out && blockIdx.x == 0 && c == 0) *len_out = uint32_t(first + n);
@@ -204,9 +242,7 @@ pool_update_fp8_kernel(const uint8_t* __restrict__ key8, const float* __restrict
   const uint32_t cnt = uint32_t(s_hi - blk_lo);
   if (c == 0) counts[b] = cnt;
   const double p = pool_max ? acc : acc / double(cnt);
-  __nv_bfloat16 parts[kMaxSeg];
-  split_bf16(float(p), int(nseg_p), parts);
-  for (uint32_t g = 0; g < nseg_p; ++g) pooled_op[b * (uint64_t(nseg_p) * kDim) + g * kDim + c] = parts[g];
+  store_pooled(b, c, float(p), pooled_op, nseg_p, pool_scale);
 }
 
 // Batch build (north-star kernel 1): the same per-column, position-ordered double accumulation, fed from shared
@@ -223,7 +259,7 @@ __global__ void __launch_bounds__(kDim)
 pool_update_staged_kernel(const void* __restrict__ key_op, const float* __restrict__ key_scale, uint32_t nseg_k,
                           uint64_t first, uint64_t n, uint32_t block_size, uint32_t pool_max, double* __restrict__ sums,
                           uint32_t* __restrict__ counts, __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p,
-                          uint32_t* __restrict__ len_out) {
+                          float* __restrict__ pool_scale, uint32_t* __restrict__ len_out) {
   extern __shared__ __align__(128) unsigned char pool_smem[];
   if (len_out && blockIdx.x == 0 && threadIdx.x == 0) *len_out = uint32_t(first + n);
   __shared__ __align__(8) uint64_t bar[2];
@@ -306,15 +342,13 @@ pool_update_staged_kernel(const void* __restrict__ key_op, const float* __restri
   const uint32_t cnt = uint32_t(s_hi - blk_lo);
   if (c == 0) counts[b] = cnt;
   const double p = pool_max ? acc : acc / double(cnt);
-  __nv_bfloat16 parts[kMaxSeg];
-  split_bf16(float(p), int(nseg_p), parts);
-  for (uint32_t g = 0; g < nseg_p; ++g) pooled_op[b * (uint64_t(nseg_p) * kDim) + g * kDim + c] = parts[g];
+  store_pooled(b, c, float(p), pooled_op, nseg_p, FP8 ? pool_scale : nullptr);
 }
 
 template <bool FP8>
 bool launch_pool_staged(const void* key_op, const float* key_scale, uint32_t nseg_k, uint64_t first, uint64_t n,
                         uint32_t block_size, uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op,
-                        uint32_t nseg_p, uint32_t* len_out, cudaStream_t stream) {
+                        uint32_t nseg_p, float* pool_scale, uint32_t* len_out, cudaStream_t stream) {
   // decode-sized appends stay on the direct kernel: nothing to stage for a handful of rows
   if (n < 32 || reinterpret_cast<uintptr_t>(key_op) % 16 != 0) return false;
   const uint32_t row_bytes = FP8 ? uint32_t(kDim) : nseg_k * uint32_t(kDim) * 2u;
@@ -323,7 +357,7 @@ bool launch_pool_staged(const void* key_op, const float* key_scale, uint32_t nse
   if (smem > 48 * 1024 && !smem_opt_in(reinterpret_cast<const void*>(kern), smem)) return false;
   const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
   kern<<<uint32_t(b1 - b0 + 1), kDim, smem, stream>>>(key_op, key_scale, nseg_k, first, n, block_size, pool_max, sums, counts,
-                                                      pooled_op, nseg_p, len_out);
+                                                      pooled_op, nseg_p, pool_scale, len_out);
   return true;
 }
 
@@ -349,16 +383,14 @@ __global__ void pool_export_kernel(const double* __restrict__ sums, const uint32
 __global__ void __launch_bounds__(kDim)
 pool_import_kernel(const double* __restrict__ src_sums, const uint32_t* __restrict__ src_counts, uint32_t dim,
                    uint32_t pool_max, double* __restrict__ sums, uint32_t* __restrict__ counts,
-                   __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p) {
+                   __nv_bfloat16* __restrict__ pooled_op, uint32_t nseg_p, float* __restrict__ pool_scale) {
   const uint32_t b = blockIdx.x, c = threadIdx.x;
   const uint32_t cnt = src_counts[b];
   const double s = c < dim ? src_sums[uint64_t(b) * dim + c] : 0.0;
   sums[uint64_t(b) * kDim + c] = s;
   if (c == 0) counts[b] = cnt;
   const double p = pool_max ? s : (cnt ? s / double(cnt) : 0.0);
-  __nv_bfloat16 parts[kMaxSeg];
-  split_bf16(float(p), int(nseg_p), parts);
-  for (uint32_t g = 0; g < nseg_p; ++g) pooled_op[b * (uint64_t(nseg_p) * kDim) + g * kDim + c] = parts[g];
+  store_pooled(b, c, float(p), pooled_op, nseg_p, pool_scale);
 }
 
 inline uint32_t blocks_for(uint64_t n, uint32_t threads) { return uint32_t((n + threads - 1) / threads); }
@@ -404,7 +436,7 @@ int launch_pool_update(const __nv_bfloat16* key_op, uint32_t nseg_k, uint64_t fi
                        uint32_t /*dim*/, uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op,
                        uint32_t nseg_p, uint32_t* len_out, cudaStream_t stream) {
   if (n == 0) return 0;
-  if (launch_pool_staged<false>(key_op, nullptr, nseg_k, first, n, block_size, pool_max, sums, counts, pooled_op, nseg_p, len_out, stream))
+  if (launch_pool_staged<false>(key_op, nullptr, nseg_k, first, n, block_size, pool_max, sums, counts, pooled_op, nseg_p, nullptr, len_out, stream))
     return 1;
   const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
   pool_update_kernel<<<uint32_t(b1 - b0 + 1), kDim, 0, stream>>>(key_op, nseg_k, first, n, block_size, pool_max, sums,
@@ -414,21 +446,22 @@ int launch_pool_update(const __nv_bfloat16* key_op, uint32_t nseg_k, uint64_t fi
 
 int launch_pool_update_fp8(const uint8_t* key8, const float* key_scale, uint64_t first, uint64_t n, uint32_t block_size,
                            uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op, uint32_t nseg_p,
-                           uint32_t* len_out, cudaStream_t stream) {
+                           float* pool_scale, uint32_t* len_out, cudaStream_t stream) {
   if (n == 0) return 0;
-  if (launch_pool_staged<true>(key8, key_scale, 1, first, n, block_size, pool_max, sums, counts, pooled_op, nseg_p, len_out, stream))
+  if (launch_pool_staged<true>(key8, key_scale, 1, first, n, block_size, pool_max, sums, counts, pooled_op, nseg_p, pool_scale, len_out, stream))
     return 1;
   const uint64_t b0 = first / block_size, b1 = (first + n - 1) / block_size;
   pool_update_fp8_kernel<<<uint32_t(b1 - b0 + 1), kDim, 0, stream>>>(key8, key_scale, first, n, block_size, pool_max, sums,
-                                                                     counts, pooled_op, nseg_p, len_out);
+                                                                     counts, pooled_op, nseg_p, pool_scale, len_out);
   return 1;
 }
 
 int launch_pool_import(const double* src_sums, const uint32_t* src_counts, uint32_t num_blocks, uint32_t dim,
                        uint32_t pool_max, double* sums, uint32_t* counts, __nv_bfloat16* pooled_op, uint32_t nseg_p,
-                       cudaStream_t stream) {
+                       float* pool_scale, cudaStream_t stream) {
   if (num_blocks == 0) return 0;
-  pool_import_kernel<<<num_blocks, kDim, 0, stream>>>(src_sums, src_counts, dim, pool_max, sums, counts, pooled_op, nseg_p);
+  pool_import_kernel<<<num_blocks, kDim, 0, stream>>>(src_sums, src_counts, dim, pool_max, sums, counts, pooled_op, nseg_p,
+                                                      pool_scale);
   return 1;
 }
 

@@ -125,7 +125,7 @@ struct RowSum {
   __device__ __forceinline__ float result() const { return keep0 + got0; }
 };
 
-// TERMS: bit (ib * 3 + ia) set <=> A segment ia is multiplied with B segment ib
+// TERMS: bit (ib * 4 + ia) set <=> A segment ia is multiplied with B segment ib
 // FP8: operands are e4m3 bytes (kind::f8f6f4, K = 32 per instruction): a 128-element row is ONE 128-byte swizzle
 // row, so a segment is a single K slab (KH = 1) where bf16 needs two (KH = 2), and a group needs one 32 KB query
 // chunk instead of two; the per-key dequantisation scale multiplies the finished row sum (scale > 0 commutes with
@@ -438,7 +438,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           if (elect_one()) {
 #pragma unroll
             for (int ia = 0; ia < NSEG_A; ++ia) {
-              if ((TERMS >> (ib * 3 + ia)) & 1u) {
+              if ((TERMS >> (ib * 4 + ia)) & 1u) {
                 const uint64_t a_tile = a_desc + uint64_t((ia * KH + kh) * (kAHalfBytes >> 4));
 #pragma unroll
                 for (int k4 = 0; k4 < 4; ++k4) {  // 32 bytes of K per instruction: 16 bf16 or 32 e4m3
@@ -674,7 +674,7 @@ int launch_variant(const ScoreArgs& args, const CUtensorMap& map_a, const CUtens
   return 1;
 }
 
-constexpr uint32_t pack_terms(uint32_t t0, uint32_t t1, uint32_t t2) { return t0 | (t1 << 3) | (t2 << 6); }
+constexpr uint32_t pack_terms(uint32_t t0, uint32_t t1, uint32_t t2) { return t0 | (t1 << 4) | (t2 << 8); }
 
 }  // namespace
 
@@ -685,6 +685,9 @@ int launch_score_tc(const ScoreArgs& args, const CUtensorMap& map_a, const CUten
   if (args.fp8) {
     if (args.nseg_a == 1 && args.nseg_b == 1 && terms == pack_terms(1, 0, 0))
       return launch_variant<1, 1, pack_terms(1, 0, 0), 2, 5, true>(args, map_a, map_b, num_sms, stream);
+    // pooled keys as four e4m3 terms (block scores of e4m3 storage): 64 KB tile, one buffer, four query stages
+    if (args.nseg_a == 4 && args.nseg_b == 1 && terms == pack_terms(15, 0, 0))
+      return launch_variant<4, 1, pack_terms(15, 0, 0), 1, 4, true>(args, map_a, map_b, num_sms, stream);
     return -1;
   }
   if (args.nseg_a == 1 && args.nseg_b == 1 && terms == pack_terms(1, 0, 0)) {

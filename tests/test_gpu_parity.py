@@ -497,6 +497,39 @@ def test_fp8_random_inputs_near_tie_rule(oracle):
     assert ex_h + near_h == Q and ex_f + near_f == Q
 
 
+@pytest.mark.parametrize("pool_mode", ["mean", "max"])
+def test_fp8_block_scores_from_e4m3_terms(oracle, monkeypatch, pool_mode):
+    """e4m3 storage scores blocks in kind::f8f6f4: pooled keys are four e4m3 terms + a power-of-two scale per block and the
+    queries stay e4m3 bytes (no bf16 copy). The result must agree with the f64 oracle like the bf16 hi|lo form does
+    (HISA_FP8_BLOCKS=0), for mean and max pooling, with an incremental append crossing a block boundary."""
+    L, Q, H, d, B = 1100, 64, 64, 128, 128
+    pos = oracle.make_positions(L, Q, "spread")
+    kw = dict(block_size=B, block_budget=4, token_budget=64)
+    if pool_mode == "max":
+        kw["pool_mode"] = 1
+    try:
+        prob = oracle.make_inputs("random", 21, L, pos, H, d, **kw)
+    except TypeError:
+        pytest.skip("oracle binding without pool_mode")
+    q8, k8, ks = quantize_problem_to_fp8(prob)
+    got = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("HISA_FP8_BLOCKS", flag)
+        with indexer_for(prob, capi.DTYPE_FP8) as ix:
+            ix.upload_keys(k8[:700], scales=ks[:700])
+            ix.pool_build()
+            ix.pool_append(k8[700:], scales=ks[700:])
+            got[flag] = ix.score_blocks(q8, prob.gates, pos)
+    (J8, ne8), (Jb, neb) = got["1"], got["0"]
+    assert np.array_equal(ne8, neb)
+    for r in range(Q):
+        want = oracle.score_blocks(prob, r)
+        assert ne8[r] == len(want)
+        scale = np.abs(want).max()
+        assert np.abs(J8[r, :ne8[r]] - want).max() <= 5e-5 * scale, f"row {r}: e4m3-term block scores"
+        assert np.abs(Jb[r, :neb[r]] - want).max() <= 5e-5 * scale, f"row {r}: bf16 hi|lo block scores"
+
+
 def test_fp8_rejects_unsupported_shapes():
     with pytest.raises(capi.HisaError) as e:
         capi.Indexer(capi.make_config(128, 4, 64, 8, 128, capi.DTYPE_FP8))
