@@ -507,7 +507,7 @@ int run_score_blocks(hisa_cuda_ctx* ctx, const Prepared& p, uint64_t q0, uint64_
   const uint32_t ntiles = Mpad / kTileRows;
   const uint32_t chunk = dense_chunk_for(ctx, nq, ntiles);
   const uint32_t nchunks = uint32_t((nq + chunk - 1) / chunk);
-  HISA_TRY(ensure(ctx, ctx->work, size_t(nchunks) * ntiles * sizeof(WorkItem)));
+  HISA_TRY(ensure(ctx, ctx->work, std::max<size_t>(size_t(nchunks) * ntiles, size_t(ctx->num_sms)) * sizeof(WorkItem)));  // >= one slot per CTA
   HISA_TRY(ensure(ctx, ctx->J, size_t(nq) * Mpad * sizeof(float)));
   uint32_t* sc = ctx->scalars.as<uint32_t>();
   StageTimer timer(ctx, kStScoreBlocks);
@@ -666,7 +666,7 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
       const uint32_t ntiles = Lpad / kTileRows;
       const uint32_t chunk = dense_chunk_for(ctx, nq, ntiles);
       const uint32_t nchunks = uint32_t((nq + chunk - 1) / chunk);
-      HISA_TRY(ensure(ctx, ctx->work, size_t(nchunks) * ntiles * sizeof(WorkItem)));
+      HISA_TRY(ensure(ctx, ctx->work, std::max<size_t>(size_t(nchunks) * ntiles, size_t(ctx->num_sms)) * sizeof(WorkItem)));  // >= one slot per CTA
       HISA_TRY(ensure(ctx, ctx->flat, size_t(nq) * Lpad * 4));
       uint32_t* sc = ctx->scalars.as<uint32_t>();
       {
@@ -735,7 +735,7 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
         const uint64_t pairs_chunk = uint64_t(chunk_list) * S;
         const uint64_t items_cap =
             uint64_t(nchunks) * (std::min<uint64_t>(M, pairs_chunk) + (split ? pairs_chunk / split : 0)) * spb;
-        HISA_TRY(ensure(ctx, ctx->work, size_t(items_cap) * sizeof(WorkItem)));
+        HISA_TRY(ensure(ctx, ctx->work, std::max<size_t>(size_t(items_cap), size_t(ctx->num_sms)) * sizeof(WorkItem)));
         HISA_TRY(ensure(ctx, ctx->pairs, size_t(nchunks) * chunk_list * S * sizeof(uint2)));
         HISA_TRY(ensure(ctx, ctx->cand, size_t(nq) * cand_cols * 4));
         // (graph replay: the variant must not depend on the current length)
@@ -1675,7 +1675,7 @@ int hisa_cuda_score_tokens(hisa_cuda_ctx* ctx, const void* queries, const float*
   const uint32_t ntiles = Lpad / kTileRows;
   const uint32_t chunk = dense_chunk_for(ctx, Q, ntiles);
   const uint32_t nchunks = uint32_t((Q + chunk - 1) / chunk);
-  HISA_TRY(ensure(ctx, ctx->work, size_t(nchunks) * ntiles * sizeof(WorkItem)));
+  HISA_TRY(ensure(ctx, ctx->work, std::max<size_t>(size_t(nchunks) * ntiles, size_t(ctx->num_sms)) * sizeof(WorkItem)));  // >= one slot per CTA
   const bool out_dev = is_device_ptr(out_scores);
   if (!out_dev) HISA_TRY(ensure(ctx, ctx->flat, size_t(Q) * Lpad * 4));
   uint32_t* sc = ctx->scalars.as<uint32_t>();

@@ -244,12 +244,21 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       ++pub;
       if (w.count == 0) pub_done = true;
     };
+    // Item ids: CTA c starts with item c (no round trip through the cursor), later ids are gridDim.x + cursor++. The item
+    // count, the first item (read speculatively: the list has room for at least gridDim.x items) and the two cursor
+    // increments for the next two ids are all in flight together, where the first item used to wait for the count, then
+    // for an atomic, then for its own load (three dependent global round trips before a CTA's first TMA request).
+    const uint32_t id_base = gridDim.x;
     if (pid == 0 && lane == 0) {
+      const uint32_t id_a = atomicAdd(a.work_cursor, 1u);
+      const uint32_t id_b = atomicAdd(a.work_cursor, 1u);
+      WorkItem w0 = a.work[blockIdx.x];
       nitems = *a.work_count;
-      publish(fetch_item(atomicAdd(a.work_cursor, 1u)));
+      if (blockIdx.x >= nitems) w0.tile = w0.first = w0.count = w0.reserved = 0;  // terminate marker
+      publish(w0);
       if (!pub_done) {
-        fw = fetch_item(atomicAdd(a.work_cursor, 1u));
-        fid = atomicAdd(a.work_cursor, 1u);
+        fw = fetch_item(id_base + id_a);
+        fid = id_base + id_b;
       }
     }
     uint32_t stage = 0, sph = 1;  // chunk ring position and the parity to wait for on b_empty
@@ -261,7 +270,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         publish(fw);
         if (!pub_done) {
           fw = fetch_item(fid);
-          fid = atomicAdd(a.work_cursor, 1u);
+          fid = id_base + atomicAdd(a.work_cursor, 1u);
         }
       }
       __syncwarp();
