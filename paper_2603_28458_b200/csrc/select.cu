@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
     kk -= scratch[41];
     lo = lo + (bin << shift);
     const uint32_t width = (shift == 0) ? 0u : ((1u << shift) - 1u);
-    hi = min(hi, lo + width);
+    hi = lo + min(hi - lo, width);  // (lo + width may pass 2^32 in the top bin: boosted keys are 0xFFFFFFFF)
     if (!use_list && lo != hi && in_bin <= uint32_t(kListCap)) {
       // the remaining levels only concern the keys of this bin: compact them once (order is irrelevant here)
       for (uint32_t i = tid; i < n; i += THREADS) {
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(kWarpSelThreads, KPL <= 16 ? 5 : 4) select_war
       kk -= __shfl_sync(FULL, c, src);
       in_range = __shfl_sync(FULL, cnt, src);
       l += bin << shift;
-      h = min(h, l + ((1u << shift) - 1u));
+      h = l + min(h - l, (1u << shift) - 1u);  // (l + width may pass 2^32 in the top bin: boosted keys are 0xFFFFFFFF)
     }
   }
   uint32_t cG = 0, cE = 0;
@@ -733,7 +733,7 @@ __global__ void __launch_bounds__(THREADS) select_cta_kernel(SelectArgs a) {
     kk -= scratch[81];
     lo = lo + (bin << shift);
     const uint32_t width = (shift == 0) ? 0u : ((1u << shift) - 1u);
-    hi = min(hi, lo + width);
+    hi = lo + min(hi - lo, width);  // (lo + width may pass 2^32 in the top bin: boosted keys are 0xFFFFFFFF)
     if (lo == hi) continue;  // exits at the top of the loop
     if (!use_list && in_bin <= uint32_t(kListCap)) {
       // the remaining work only concerns the keys of this bin: compact them once (order is irrelevant here)
@@ -1108,7 +1108,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? 4 : 2) select_tok_ke
     kk -= scratch[81];
     lo = lo + (bin << shift);
     const uint32_t width = (shift == 0) ? 0u : ((1u << shift) - 1u);
-    hi = min(hi, lo + width);
+    hi = lo + min(hi - lo, width);  // (lo + width may pass 2^32 in the top bin: boosted keys are 0xFFFFFFFF)
   }
 
   // ---- ordered output -------------------------------------------------------------------------------------

@@ -117,6 +117,32 @@ def test_select_blocks_on_given_scores_bit_exact(oracle, tb, ffl, fib):
         assert (blocks[r, nb[r]:] == -1).all()
 
 
+@pytest.mark.parametrize("M", [133, 1500, 12000])   # warp-per-row, CTA-per-row and multi-pass kernels
+@pytest.mark.parametrize("m", [1, 2, 3])
+def test_select_blocks_forced_in_budget_tiny_budget(oracle, M, m):
+    """forced_in_budget boosts the sink and local block to the largest key (0xFFFFFFFF). With a budget of one to three
+    blocks the threshold lies in the TOP radix bin, whose upper edge lo + width passes 2^32: a stress seed (B=16, m=2,
+    133 blocks) hit exactly that in the range narrowing. All-negative, all-equal and wide-range rows included."""
+    rng = np.random.default_rng(5 + M + m)
+    rows, B = 48, 8
+    ne = rng.integers(1, M + 1, rows).astype(np.uint32)
+    ne[:5] = [1, 2, 3, M, M - 1]
+    J = (rng.standard_normal((rows, M)) * 10.0 ** rng.integers(-3, 4, (rows, 1))).astype(np.float32)
+    J[5] = -np.abs(J[5])
+    J[6] = 1.5
+    J[7, ::2] = 1e30
+    for tb in (0, 1):
+        cfg = capi.make_config(B, m, m * B, 4, 8, capi.DTYPE_F32, force_first_last=True, forced_in_budget=True, tie_break=tb)
+        with capi.Indexer(cfg) as ix:
+            blocks, nb = ix.select_blocks(J, ne)
+        p = oracle.Problem(np.zeros((1, 1, 1)), np.zeros((1, 1)), np.zeros((1, 1)), np.zeros(1, np.uint32), block_size=B,
+                           block_budget=m, token_budget=m * B, force_first_last=True, forced_in_budget=True, tie_break=tb)
+        for r in range(rows):
+            t = (int(ne[r]) - 1) * B + 3
+            want = oracle.select_blocks(J[r, :ne[r]].astype(np.float64), np.arange(ne[r]), p, t)
+            assert blocks[r, :nb[r]].tolist() == want.tolist(), f"row {r} E={ne[r]} tb={tb}"
+
+
 # ------------------------------------------------------------------------------------------ scorers
 @pytest.mark.parametrize("scorer", [capi.SCORER_SIMT, capi.SCORER_TENSOR])
 @pytest.mark.parametrize("dtype", [capi.DTYPE_BF16, capi.DTYPE_F32])
