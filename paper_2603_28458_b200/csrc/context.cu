@@ -158,8 +158,13 @@ int fail(hisa_cuda_ctx* ctx, int code, const char* fmt, ...) {
     if (rc__ != HISA_OK) return rc__; \
   } while (0)
 
+void drop_graph(hisa_cuda_ctx* ctx);
+
 int ensure(hisa_cuda_ctx* ctx, DevBuf& b, size_t bytes) {
   if (bytes <= b.cap) return HISA_OK;
+  // a captured decode graph holds the addresses of the workspace buffers as kernel arguments: a buffer that moves (a larger
+  // call between two decode steps) must take the graph with it, or the next replay reads and writes freed memory
+  drop_graph(ctx);
   if (b.p) {
     CU_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     CU_TRY(ctx, cudaFree(b.p));

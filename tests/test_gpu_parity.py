@@ -986,3 +986,41 @@ def test_decode_loop_replays_one_graph(oracle):
     got = {"idx": idx, "count": cnt, "cand": cand, "blocks": want["blocks"], "nblocks": want["nblocks"]}
     ex, near, rec = compare_selection(oracle, prob, "hisa", got, np.arange(64), BF16_RTOL)
     assert rec >= 0.999
+
+
+def test_decode_graph_survives_a_larger_call_in_between(oracle):
+    """A captured decode graph holds the workspace addresses. A larger call between two decode steps (here a 3000-row
+    hierarchical and a flat selection) grows and moves those buffers: the next decode step must not replay the stale graph.
+    Every decode step is compared with a fresh context's plain call. (The stale replay wrote to freed memory, which only
+    compute-sanitizer reports reliably: scripts/sanitize.sh runs this test under memcheck.)"""
+    L0, B, m, k = 6000, 128, 8, 512
+    rows = np.full(64, 2 ** 31 - 1, np.uint32)
+    prob, qb, kb = _numpy_problem(oracle, L0 + 16, rows, 17, B, m, k)
+    big_rows = np.arange(3000, dtype=np.uint32)
+    bprob, bq, _ = _numpy_problem(oracle, L0 + 16, big_rows, 18, B, m, k)
+    cfg = capi.make_config(B, m, k, 64, 128, capi.DTYPE_BF16)
+    with capi.Indexer(cfg, 0) as ix, capi.Indexer(cfg, 0) as ref:
+        ix.upload_keys(kb[:L0])
+        ix.pool_build()
+        dq, dw, dp = ix.device_alloc(qb.nbytes), ix.device_alloc(prob.gates.nbytes), ix.device_alloc(rows.nbytes)
+        d_idx, d_cnt = ix.device_alloc(64 * k * 4), ix.device_alloc(64 * 4)
+        d_key = ix.device_alloc(16 * 128 * 2)
+        ix.memcpy(dq, qb, qb.nbytes), ix.memcpy(dw, prob.gates, prob.gates.nbytes), ix.memcpy(dp, rows, rows.nbytes)
+        ix.memcpy(d_key, kb[L0:], 16 * 128 * 2)
+
+        def decode_step(s):
+            ix.pool_append(d_key + s * 256, n=1, key_dim=128)
+            ix.hisa_select_raw(dq, dw, dp, 64, d_idx, d_cnt, None, None, None)
+            ix.synchronize()
+            idx, cnt = np.empty((64, k), np.int32), np.empty(64, np.uint32)
+            ix.memcpy(idx, d_idx, idx.nbytes), ix.memcpy(cnt, d_cnt, cnt.nbytes)
+            ref.upload_keys(kb[:L0 + s + 1])
+            want = ref.hisa_select(qb, prob.gates, rows)
+            assert np.array_equal(idx, want["idx"]) and np.array_equal(cnt, want["count"]), f"decode step {s} differs"
+
+        for s in range(5):
+            decode_step(s)                       # the graph is captured and replayed
+        ix.hisa_select(bq, bprob.gates, big_rows)  # grows the work lists, block scores, candidate scores ...
+        ix.dsa_select(bq, bprob.gates, big_rows)   # ... and the flat logits
+        for s in range(5, 10):
+            decode_step(s)
