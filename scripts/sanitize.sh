@@ -6,7 +6,7 @@
 #               hazards on the scorer's meta slots are expected and not a finding.
 mkdir -p gpurun_out
 timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests -m gpu -q -x -p no:cacheprovider \
-  -k "lattice_inputs_bit_exact and 1-shape1 or fp8_lattice or top_k_on_given_scores and 9000 or pool_append or decode_placement or tmem_tile_variant or decode_config_c5_128k or survives_a_larger_call or forced_in_budget_tiny" \
+  -k "lattice_inputs_bit_exact and 1-shape1 or fp8_lattice or top_k_on_given_scores and 9000 or pool_append or decode_placement or tmem_tile_variant or decode_config_c5_128k or survives_a_larger_call or forced_in_budget_tiny or random_api_sessions" \
   > gpurun_out/memcheck.log 2>&1; echo "memcheck rc=$?"; tail -3 gpurun_out/memcheck.log
 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_attention.py -m gpu -q -x \
   -p no:cacheprovider -k "not full_size" > gpurun_out/memcheck_attend.log 2>&1; echo "memcheck (consumer) rc=$?"; tail -3 gpurun_out/memcheck_attend.log

@@ -1024,3 +1024,72 @@ def test_decode_graph_survives_a_larger_call_in_between(oracle):
         ix.dsa_select(bq, bprob.gates, big_rows)   # ... and the flat logits
         for s in range(5, 10):
             decode_step(s)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp8"])
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("HISA_STRESS_SEEDS", "3"))))
+def test_random_api_sessions_equal_fresh_contexts(oracle, seed, dtype):
+    """State machine check: a long-lived context driven through a seeded random sequence of operations (key appends of
+    1..300 tokens, re-uploads of a different length, hierarchical / flat / block-sparse selections from host buffers with
+    random row counts and positions, decode-style repeated calls on fixed device buffers that get captured into a graph)
+    must return, at every selection, exactly what a FRESH context returns for the same keys and queries: stale graphs,
+    stale tail blocks, stale workspace or operand state would all show up as a difference."""
+    rng = np.random.default_rng(7000 + seed)
+    B = int(rng.choice([32, 64, 128]))
+    m = int(rng.integers(2, 9))
+    k = int(rng.integers(8, m * B + 1))
+    Lmax = 5000
+    keys_f = rng.standard_normal((Lmax, 128), dtype=np.float32)
+    if dtype == "bf16":
+        code = capi.DTYPE_BF16
+        kb_all, ks_all = capi.f32_to_bf16_bits(keys_f), None
+        quant = capi.f32_to_bf16_bits
+    else:
+        code = capi.DTYPE_FP8
+        ks_all = (np.abs(keys_f).max(axis=1) / 448.0).astype(np.float32)
+        kb_all = capi.f32_to_e4m3_bits(keys_f / ks_all[:, None])
+        quant = capi.f32_to_e4m3_bits
+    cfg = capi.make_config(B, m, k, 64, 128, code)
+    L = int(rng.integers(B + 1, 1500))
+
+    def fresh_select(which, q, w, pos, Lnow):
+        with capi.Indexer(cfg, 0) as ref:
+            ref.upload_keys(kb_all[:Lnow], scales=None if ks_all is None else ks_all[:Lnow])
+            return ref._select(which, q, w, pos)
+
+    with capi.Indexer(cfg, 0) as ix:
+        ix.upload_keys(kb_all[:L], scales=None if ks_all is None else ks_all[:L])
+        # fixed device buffers of the decode-style calls
+        Qd = int(rng.choice([1, 7, 64]))
+        qd = quant(rng.standard_normal((Qd, 64, 128), dtype=np.float32) * (1.0 if dtype == "bf16" else 3.0))
+        wd = rng.uniform(0.5, 1.5, (Qd, 64)).astype(np.float32)
+        pd = np.full(Qd, 2 ** 31 - 1, np.uint32)
+        dq, dw, dp = ix.device_alloc(qd.nbytes), ix.device_alloc(wd.nbytes), ix.device_alloc(pd.nbytes)
+        d_idx, d_cnt = ix.device_alloc(Qd * k * 4), ix.device_alloc(Qd * 4)
+        ix.memcpy(dq, qd, qd.nbytes), ix.memcpy(dw, wd, wd.nbytes), ix.memcpy(dp, pd, pd.nbytes)
+        for step in range(24):
+            op = int(rng.integers(0, 10))
+            if op <= 2 and L < Lmax - 300:                                   # append
+                n = int(rng.choice([1, 1, 1, 5, 37, 300]))
+                ix.pool_append(kb_all[L:L + n], scales=None if ks_all is None else ks_all[L:L + n])
+                L += n
+            elif op == 3:                                                    # re-upload another length
+                L = int(rng.integers(B + 1, Lmax - 400))
+                ix.upload_keys(kb_all[:L], scales=None if ks_all is None else ks_all[:L])
+            elif op <= 6:                                                    # decode-style call on the fixed device buffers
+                ix.hisa_select_raw(dq, dw, dp, Qd, d_idx, d_cnt, None, None, None)
+                ix.synchronize()
+                idx, cnt = np.empty((Qd, k), np.int32), np.empty(Qd, np.uint32)
+                ix.memcpy(idx, d_idx, idx.nbytes), ix.memcpy(cnt, d_cnt, cnt.nbytes)
+                want = fresh_select("hisa", qd, wd, pd, L)
+                assert np.array_equal(idx, want["idx"]) and np.array_equal(cnt, want["count"]), f"step {step}: decode call, L={L}"
+            else:                                                            # a selection from host buffers
+                which = ["hisa", "dsa", "block"][int(rng.integers(0, 3))]
+                Q = int(rng.choice([1, 3, 64, 200, 2100]))
+                q = quant(rng.standard_normal((Q, 64, 128), dtype=np.float32) * (1.0 if dtype == "bf16" else 3.0))
+                w = rng.uniform(-1.0, 1.5, (Q, 64)).astype(np.float32)
+                pos = rng.integers(0, L + 1, Q).astype(np.uint32)
+                got = ix._select(which, q, w, pos)
+                want = fresh_select(which, q, w, pos, L)
+                for key in ("idx", "count"):
+                    assert np.array_equal(got[key], want[key]), f"step {step}: {which} {key}, Q={Q} L={L}"
