@@ -129,8 +129,17 @@ class MultiIndexer {
 // (strategy, length). FixedBudget keeps cfg.block_budget; Ratio recomputes m per length so that M : m = ratio : 1
 // (m = ceil(ceil(L/B) / ratio), raised to keep m*B >= k).
 enum class SweepMode { FixedBudget, Ratio };
+// storage: how keys and queries are held on the device (F32 = what hisa::run_bench uses: the reference stores f32).
+// time_base: what wall_ns_* measure. Call = the whole batched call, host containers in, host results out (the copies of
+// the f32 IndexerInputs over PCIe dominate calls of ~1000 rows); Kernels = the device time of the indexer's kernels only
+// (operands resident, as the paper times its kernels).
+enum class TimeBase { Call, Kernels };
 std::vector<BenchRecord> run_bench_sweep(const HisaConfig& cfg, std::span<const uint32_t> lengths, uint32_t num_queries,
                                          uint64_t seed, std::span<const Strategy> strategies, SweepMode mode,
-                                         uint32_t ratio = 4, const BenchOptions& options = {});
+                                         uint32_t ratio = 4, const BenchOptions& options = {},
+                                         Storage storage = Storage::F32, TimeBase time_base = TimeBase::Call);
+// hisa::run_bench (hisa/bench.hpp:53) with the device storage and the time base chosen by the caller
+BenchRecord run_bench(const HisaConfig& cfg, uint32_t seq_len, uint32_t num_queries, uint64_t seed, Strategy strategy,
+                      const BenchOptions& options, Storage storage, TimeBase time_base = TimeBase::Call);
 
 }  // namespace hisa::gpu

@@ -874,9 +874,14 @@ SelectionResult block_sparse_select(const IndexerInputs& in, const BlockSummaryC
 // ==================================================================================================
 BenchRecord run_bench(const HisaConfig& cfg, uint32_t seq_len, uint32_t num_queries, uint64_t seed, Strategy strategy,
                       const BenchOptions& opt) {
+  return gpu::run_bench(cfg, seq_len, num_queries, seed, strategy, opt, gpu::Storage::F32);
+}
+
+BenchRecord gpu::run_bench(const HisaConfig& cfg, uint32_t seq_len, uint32_t num_queries, uint64_t seed, Strategy strategy,
+                           const BenchOptions& opt, Storage storage, TimeBase time_base) {
   Rng rng(seed);
   const IndexerInputs in = make_random_inputs(rng, seq_len, num_queries, cfg.num_heads, cfg.dim, opt.placement);
-  gpu::Indexer ix(cfg, gpu::Storage::F32);
+  gpu::Indexer ix(cfg, storage);
   ix.enable_timing(true);
   ix.set_keys(in.keys_raw());
   BenchRecord rec;
@@ -889,7 +894,10 @@ BenchRecord run_bench(const HisaConfig& cfg, uint32_t seq_len, uint32_t num_quer
     if (strategy == Strategy::Dsa) ix.dsa_select_batch(in, c);
     else if (strategy == Strategy::Hisa) ix.hisa_select_batch(in, c);
     else ix.block_sparse_select_batch(in, c);
-    return ix.last_times().total_ms;
+    const auto t = ix.last_times();
+    if (time_base == TimeBase::Kernels)
+      return t.score_blocks_ms + t.select_blocks_ms + t.invert_ms + t.score_tokens_ms + t.top_k_ms;
+    return t.total_ms;
   };
   if (opt.timing) {
     for (uint32_t i = 0; i < opt.warmup; ++i) once(nullptr);
@@ -921,7 +929,7 @@ namespace gpu {
 // Fig. 2's two panels (SPEC.md:462 `bench --mode fixed-budget | ratio`)
 std::vector<BenchRecord> run_bench_sweep(const HisaConfig& cfg, std::span<const uint32_t> lengths, uint32_t num_queries,
                                          uint64_t seed, std::span<const Strategy> strategies, SweepMode mode, uint32_t ratio,
-                                         const BenchOptions& options) {
+                                         const BenchOptions& options, Storage storage, TimeBase time_base) {
   if (mode == SweepMode::Ratio && ratio == 0) throw Error("run_bench_sweep: ratio must be at least 1");
   std::vector<BenchRecord> out;
   for (uint32_t L : lengths) {
@@ -936,7 +944,7 @@ std::vector<BenchRecord> run_bench_sweep(const HisaConfig& cfg, std::span<const 
     c.forced_in_budget = cfg.forced_in_budget;
     c.tie_break = cfg.tie_break;
     c.pool_mode = cfg.pool_mode;
-    for (Strategy s : strategies) out.push_back(run_bench(c, L, num_queries, seed, s, options));
+    for (Strategy s : strategies) out.push_back(gpu::run_bench(c, L, num_queries, seed, s, options, storage, time_base));
   }
   return out;
 }
