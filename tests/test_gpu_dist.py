@@ -124,3 +124,36 @@ def test_cpp_driver_program_checks_itself():
                            capture_output=True, text=True, timeout=600)
         print(r.stdout[-1500:], r.stderr[-1500:])
         assert r.returncode == 0 and '"bit_equal_to_one_gpu": true' in r.stdout
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("HISA_STRESS_SEEDS", "4"))))
+def test_random_shard_plans_equal_single_context(oracle, seed):
+    """Seeded random row counts (not multiples of the 512-row tile), world sizes up to 8 logical ranks, slice counts,
+    budgets on both sides of the warp / CTA top-k boundary, random (repeated, unordered) query positions: the matrix
+    every rank ends up with must equal the single-context result bit for bit."""
+    rng = np.random.default_rng(300 + seed)
+    L = int(rng.integers(600, 5000))
+    Q = int(rng.integers(1, 4000))
+    world = int(rng.choice([2, 3, 5, 8]))
+    slices = int(rng.integers(1, 6))
+    B = int(rng.choice([64, 128]))
+    m = int(rng.choice([2, 6, 20, 40]))
+    k = int(rng.integers(1, m * B + 1))
+    strategy = "hisa" if rng.integers(0, 2) else "dsa"
+    pos = rng.integers(0, L, Q).astype(np.uint32)
+    prob = oracle.make_inputs("random", 40 + seed, L, pos, 64, 128, block_size=B, block_budget=m, token_budget=k)
+    qb, kb = round_problem_to_bf16(prob)
+    want = _single(prob, qb, kb, strategy)
+    cfg = capi.make_config(B, m, k, 64, 128, capi.DTYPE_BF16)
+    with capi.Dist(cfg, devices=[0] * world) as dist:
+        dist.upload_keys(kb, L)
+        rows = [capi.dist_plan(Q, world, r) for r in range(world)]
+        assert sorted(np.concatenate(rows).tolist()) == list(range(Q))
+        qs = [np.ascontiguousarray(qb[r]) for r in rows]
+        ws = [np.ascontiguousarray(prob.gates[r]) for r in rows]
+        ps = [np.ascontiguousarray(prob.positions[r]) for r in rows]
+        dist.select(capi.DIST_HISA if strategy == "hisa" else capi.DIST_DSA, qs, ws, ps, Q, num_slices=slices)
+        for local in {0, world - 1, int(rng.integers(0, world))}:
+            idx, cnt = dist.fetch(Q, local)
+            assert np.array_equal(cnt, want["count"]), f"rank {local}: counts differ (Q={Q} world={world} slices={slices})"
+            assert np.array_equal(idx, want["idx"]), f"rank {local}: rows differ (Q={Q} world={world} slices={slices} m={m} k={k})"
