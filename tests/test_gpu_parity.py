@@ -1059,10 +1059,14 @@ def test_random_api_sessions_equal_fresh_contexts(oracle, seed, dtype, monkeypat
 
     # odd seeds: the long-lived context stages host buffers in slices of 160 rows (H2D / kernels / D2H pipelined over
     # three streams), the fresh contexts do not: sliced and unsliced calls must agree as well
+    # seeds = 2 mod 3: the smallest workspace the context accepts (16 MiB), so larger calls run in several passes of rows
     if seed % 2:
         monkeypatch.setenv("HISA_PIPE_ROWS", "160")
+    if seed % 3 == 2:
+        monkeypatch.setenv("HISA_WORKSPACE_MB", "16")
     ix_cm = capi.Indexer(cfg, 0)
     monkeypatch.delenv("HISA_PIPE_ROWS", raising=False)
+    monkeypatch.delenv("HISA_WORKSPACE_MB", raising=False)
     with ix_cm as ix:
         ix.upload_keys(kb_all[:L], scales=None if ks_all is None else ks_all[:L])
         # fixed device buffers of the decode-style calls
