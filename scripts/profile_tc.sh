@@ -1,6 +1,6 @@
 #!/bin/bash
 # Runs on the GPU box: full ncu capture of the scorer launches of one hisa_select call (stage 1 + stage 2).
-# PROF_TAG names the output; HISA_TC_DEBUG passes through to the library (timing experiments).
+# PROF_TAG names the output; environment knobs (HISA_TC_ATMEM, HISA_TC_PRODUCERS ...) pass through to the library.
 mkdir -p gpurun_out
 TAG=${PROF_TAG:-score_tc}
 BENCH="python bench.py --e2e-steps 0 --no-cpu-baseline"
