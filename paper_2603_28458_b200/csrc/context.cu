@@ -791,6 +791,7 @@ int select_core(hisa_cuda_ctx* ctx, Strategy strat, const void* queries, const f
           s.sel_stride = S;
           s.dyn_len = ctx->dyn ? ctx->dlen.as<uint32_t>() : nullptr;
           s.tie_break = c.tie_break;
+          s.force_first_last = c.force_first_last;  // lets the kernel derive a row's last selected block from its position
           s.out_idx = idx_dst;
           s.out_stride = out_width;
           s.out_width = out_width;

@@ -924,7 +924,9 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? 4 : 2) select_tok_ke
     const uint32_t t = min(a.pos[row], seq_len_of(a) - 1);
     ns = a.nsel[row];
     sel_row = a.sel + uint64_t(row) * a.sel_row_stride;
-    const uint32_t lastb = uint32_t(sel_row[ns - 1]);
+    // the last selected block: with force_first_last it is the local block (the last block the summaries cover at or
+    // before t), known without reading the list: one dependent global load less before the row's copy can be requested
+    const uint32_t lastb = a.force_first_last ? min(t / B, num_blocks_of(a) - 1) : uint32_t(sel_row[ns - 1]);
     n = (ns - 1) * B + min(B, t - lastb * B + 1);
   } else {
     n = a.n_in[row];
