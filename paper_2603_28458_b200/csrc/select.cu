@@ -92,7 +92,7 @@ __device__ __forceinline__ uint32_t block_reduce_max(uint32_t v, uint32_t* scrat
 }
 
 template <int THREADS, bool SMEM_KEYS>
-__global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
+__global__ void __launch_bounds__(THREADS, THREADS == 1024 ? 2 : 1) select_rows_kernel(SelectArgs a) {
   extern __shared__ __align__(16) uint32_t smem_u[];
   uint32_t* hist = smem_u;                // [kBins]
   uint32_t* scratch = smem_u + kBins;     // [64]
@@ -180,6 +180,22 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
       kmin = min(kmin, key);
       kmax = max(kmax, key);
     }
+  } else if (!SMEM_KEYS && a.vec_ok && !boost) {
+    // rows too long for shared memory: every pass streams the row from L2 / HBM. 16-byte loads (four scores per request):
+    // the scalar version spent 70 % of its stall samples waiting for 4-byte loads (long scoreboard + LSU queue throttle)
+    const float4* s4 = reinterpret_cast<const float4*>(srow);
+    const uint32_t n4 = n >> 2;
+    for (uint32_t i = tid; i < n4; i += THREADS) {
+      const float4 v = __ldg(s4 + i);
+      const uint32_t kx = score_key(v.x), ky = score_key(v.y), kz = score_key(v.z), kw = score_key(v.w);
+      kmin = min(min(kmin, kx), min(min(ky, kz), kw));
+      kmax = max(max(kmax, kx), max(max(ky, kz), kw));
+    }
+    for (uint32_t i = (n4 << 2) + tid; i < n; i += THREADS) {
+      const uint32_t key = score_key(srow[i]);
+      kmin = min(kmin, key);
+      kmax = max(kmax, key);
+    }
   } else {
     for (uint32_t i = tid; i < n; i += THREADS) {
       const uint32_t key = raw_key(i);
@@ -188,6 +204,24 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
       kmax = max(kmax, key);
     }
   }
+  const bool vec_g = !SMEM_KEYS && a.vec_ok && !boost;  // the passes below read the row with 16-byte loads as well
+  // f(i, key) for every candidate, lanes on consecutive 16-byte chunks (order across threads is irrelevant to the caller)
+  auto for_each_strided = [&](auto&& f) {
+    if (vec_g) {
+      const float4* s4 = reinterpret_cast<const float4*>(srow);
+      const uint32_t n4 = n >> 2;
+      for (uint32_t i = tid; i < n4; i += THREADS) {
+        const float4 v = __ldg(s4 + i);
+        f(4 * i + 0, score_key(v.x));
+        f(4 * i + 1, score_key(v.y));
+        f(4 * i + 2, score_key(v.z));
+        f(4 * i + 3, score_key(v.w));
+      }
+      for (uint32_t i = (n4 << 2) + tid; i < n; i += THREADS) f(i, score_key(srow[i]));
+    } else {
+      for (uint32_t i = tid; i < n; i += THREADS) f(i, key_at(i));
+    }
+  };
   uint32_t lo = block_reduce_min<THREADS>(kmin, scratch);
   uint32_t hi = block_reduce_max<THREADS>(kmax, scratch);
   __syncthreads();
@@ -212,10 +246,9 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
         if (key >= lo && key <= hi) atomicAdd(&hist[(key - lo) >> shift], 1u);
       }
     } else {
-      for (uint32_t i = tid; i < n; i += THREADS) {
-        const uint32_t key = key_at(i);
+      for_each_strided([&](uint32_t, uint32_t key) {
         if (key >= lo && key <= hi) atomicAdd(&hist[(key - lo) >> shift], 1u);
-      }
+      });
     }
     __syncthreads();
     constexpr int BPT = kBins / THREADS;
@@ -247,10 +280,9 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
     hi = lo + min(hi - lo, width);  // (lo + width may pass 2^32 in the top bin: boosted keys are 0xFFFFFFFF)
     if (!use_list && lo != hi && in_bin <= uint32_t(kListCap)) {
       // the remaining levels only concern the keys of this bin: compact them once (order is irrelevant here)
-      for (uint32_t i = tid; i < n; i += THREADS) {
-        const uint32_t key = key_at(i);
+      for_each_strided([&](uint32_t, uint32_t key) {
         if (key >= lo && key <= hi) list[atomicAdd(&scratch[43], 1u)] = key;
-      }
+      });
       use_list = true;
       list_n = in_bin;
     }
@@ -260,14 +292,39 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
   const uint32_t need = kk;  // ties (key == T) to take
 
   // ---- ordered compaction over blocked segments ---------------------------------------------------
-  const uint32_t ipt = ((n + THREADS - 1) / THREADS) | 1u;  // odd: conflict-free strided smem walks
-  const uint32_t s0 = min(n, tid * ipt), s1 = min(n, s0 + ipt);
+  // thread t owns the contiguous candidates [s0, s1); global rows: whole 16-byte chunks per thread, the ragged tail (< 4
+  // candidates) goes to the last thread, whose segment is the last one anyway
+  uint32_t s0, s1;
+  if (vec_g) {
+    const uint32_t n4 = n >> 2, q4 = (n4 + THREADS - 1) / THREADS;
+    s0 = 4u * min(n4, tid * q4);
+    s1 = tid == THREADS - 1 ? n : 4u * min(n4, tid * q4 + q4);
+  } else {
+    const uint32_t ipt = ((n + THREADS - 1) / THREADS) | 1u;  // odd: conflict-free strided smem walks
+    s0 = min(n, tid * ipt);
+    s1 = min(n, s0 + ipt);
+  }
+  // f(i, key) for the thread's candidates in ascending order
+  auto for_each_owned = [&](auto&& f) {
+    if (vec_g) {
+      const uint32_t v1 = s0 + ((s1 - s0) & ~3u);  // end of the whole chunks (s0 is a multiple of 4)
+      for (uint32_t i = s0; i < v1; i += 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(srow + i));
+        f(i + 0, score_key(v.x));
+        f(i + 1, score_key(v.y));
+        f(i + 2, score_key(v.z));
+        f(i + 3, score_key(v.w));
+      }
+      for (uint32_t i = v1; i < s1; ++i) f(i, score_key(srow[i]));
+    } else {
+      for (uint32_t i = s0; i < s1; ++i) f(i, key_at(i));
+    }
+  };
   uint32_t cG = 0, cE = 0;
-  for (uint32_t i = s0; i < s1; ++i) {
-    const uint32_t key = key_at(i);
+  for_each_owned([&](uint32_t, uint32_t key) {
     cG += key > T;
     cE += key == T;
-  }
+  });
   uint32_t totG, totE;
   const uint32_t gBefore = block_scan_excl<THREADS>(cG, scratch, totG);
   const uint32_t eBefore = block_scan_excl<THREADS>(cE, scratch, totE);
@@ -285,15 +342,14 @@ __global__ void __launch_bounds__(THREADS) select_rows_kernel(SelectArgs a) {
   const uint32_t tiesBefore = eBefore > skip ? min(eBefore - skip, need) : 0u;
   uint32_t o = gBefore + tiesBefore + add_first;
   uint32_t e = eBefore;
-  for (uint32_t i = s0; i < s1; ++i) {
-    const uint32_t key = key_at(i);
+  for_each_owned([&](uint32_t i, uint32_t key) {
     bool emit = key > T;
     if (key == T) {
       emit = (e >= skip) && (e < skip + need);
       ++e;
     }
     if (emit) orow[o++] = position_of(i);
-  }
+  });
   const uint32_t count = totG + need + add_first + add_last;
   if (add_first && tid == 0) orow[0] = position_of(0);
   if (add_last && tid == 0) orow[count - 1] = position_of(n - 1);
