@@ -773,7 +773,10 @@ def run_b200(a, rank, world, local_rank):
                        "l2": f"inputs larger than L2 (q is {q_gib:.1f} GiB per step)",
                        "sharding": f"query tiles of {TILE_ROWS} rows round-robin over ranks; keys NCCL-broadcast; "
                                    "indices all-gathered inside the step" if world > 1 else "single GPU"},
-            "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
+            # NVML is sampled every 20 ms and lags a timed region of ~90 ms; the clock the scorer kernels really ran at
+            # (longest CTA lifetime in cycles / kernel time, from the instrumented pass) is reported beside it
+            "clocks": dict(clocks.summary(), sm_mhz_in_scorer_kernels={kk: vv.get("sm_mhz_in_kernel") for kk, vv in stalls.items()}),
+            "e2e": e2e, "gpu_launches": launches,
             "roofline": roofline, "stage_rooflines": stage_rooflines, "cpu_baseline": cpu, "flat_dsa": flat,
             "stages_ms_per_step": per_call, "consumer_sparse_attend": consumer,
             "scorer_stall_fraction_of_cta_time": stalls,
